@@ -1,0 +1,175 @@
+/* momg_gpu -- C ABI of the B200-native NMG / fast-sweeping hot path.
+ *
+ * This is the drop-in boundary.  The reference has no FFI
+ * or plugin registry: its boundary is the set of C++ free functions in
+ * namespace momg that the host driver calls.  Each entry point below replaces
+ * exactly one of them (reference file:line cited); plain pointers, sizes and
+ * status codes only -- no C++ or torch types cross this line.
+ *
+ * Device residency: a momg_field is one grid level living in B200 HBM
+ * (coefficients [cells][NP] cell-major with NP = N rounded up to 4 doubles,
+ * params [cells][4]).  Host arrays passed to upload/download use the
+ * reference's host order: coeffs[(j*nx+i)*N + k], params[(j*nx+i)*4 + q]
+ * (grid.hpp:64, moment_rep.hpp:16-32).  All work is FP64 and runs on the
+ * library's CUDA stream (momg_set_stream); calls are stream-ordered and only
+ * the ones that return host scalars or report errors synchronise.
+ *
+ * Errors: every function returns a momg status (0 = OK) and fills *err
+ * (nullable).  Codes mirror the reference exception hierarchy
+ * (types.hpp:20-57); the host wrappers rethrow the matching exception type so
+ * solve_steady's catch logic (multigrid.cpp:289-300) is unchanged.
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns MOMG_ERR_NO_DEVICE.
+ */
+#ifndef MOMG_GPU_H
+#define MOMG_GPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum momg_status {
+  MOMG_OK = 0,
+  MOMG_NONPHYSICAL_STATE = 1, /* NonphysicalState   (types.hpp:33) */
+  MOMG_SOLVER_ERROR = 2,      /* SolverError        (types.hpp:54) */
+  MOMG_ERROR = 3,             /* Error              (types.hpp:20), e.g. grad_normalize cap */
+  MOMG_NON_SPD = 4,           /* NonSpdTensor       (types.hpp:46) */
+  MOMG_CONFIG = 5,            /* ConfigError        (types.hpp:26) */
+  MOMG_NONCONVERGENCE = 6,    /* NonConvergence     (multigrid.hpp:89-97) */
+  MOMG_ERR_NO_DEVICE = 100,   /* no CUDA device / extension unusable */
+  MOMG_ERR_CUDA = 101,        /* CUDA runtime failure */
+  MOMG_ERR_ARG = 102          /* invalid argument (null handle, shape mismatch) */
+};
+
+typedef struct momg_err {
+  int code;
+  int i, j;        /* failing cell when known, else -1 */
+  char msg[256];
+} momg_err;
+
+/* Grid2D (grid.hpp:12-37): per-cell sizes and centres, host pointers. */
+typedef struct momg_grid {
+  int nx, ny;
+  double Lx, Ly;
+  const double *dx, *dy, *xc, *yc;
+} momg_grid;
+
+enum { MOMG_BGK = 0, MOMG_ES_BGK = 1, MOMG_SHAKHOV = 2 };
+
+/* SolveContext (single_level.hpp:27-34): walls left, right, bottom, top. */
+typedef struct momg_ctx {
+  int M;               /* moment order (IndexSet order) */
+  int space_order;     /* SpatialScheme.order, 1 or 2 (spatial.hpp:16-22) */
+  double c_bound;      /* SpatialScheme.c_bound = max_hermite_root(M+1) */
+  double cfl;          /* CflPolicy.cfl */
+  double cfl_c_bound;  /* CflPolicy.c_bound */
+  int collision;       /* CollisionModel.kind */
+  double prandtl;      /* CollisionModel.prandtl */
+  double knudsen;      /* GasParams.knudsen */
+  double viscosity_index; /* GasParams.viscosity_index */
+  double wall_speed[4];
+  double wall_theta[4];
+  int threads;         /* accepted for API parity; ignored (device-parallel) */
+} momg_ctx;
+
+/* CyclePolicy + SolverOptions (multigrid.hpp:30-35, 101-107). */
+typedef struct momg_solver_opts {
+  int kind;            /* 0 euler, 1 fs, 2 nmg (SolverKind) */
+  double tol;
+  int max_iterations;  /* 0: 200 nmg, 100000 fs/euler */
+  int levels;          /* 0: auto (GridHierarchy::build) */
+  int s1, s2, s3, gamma;
+} momg_solver_opts;
+
+/* SolveReport (multigrid.hpp:78-87); history = rel_residual per iteration. */
+typedef struct momg_report {
+  int converged;
+  int iterations;
+  double r0_norm;
+  double final_norm;
+  double final_ratio;
+  long long work;      /* fast-sweeping cell evaluations (WorkStats) */
+  double seconds;
+  int history_len;
+  double* history;     /* caller buffer, capacity history_cap (nullable) */
+  int history_cap;
+} momg_report;
+
+typedef struct momg_field momg_field; /* opaque device-resident level */
+
+/* ---- runtime ---------------------------------------------------------- */
+int momg_init(int device, momg_err* err);          /* select device, create stream */
+int momg_set_stream(void* cuda_stream);            /* use an external stream (nullable = own) */
+void* momg_get_stream(void);
+int momg_synchronize(momg_err* err);
+const char* momg_version(void);
+int momg_supported_order(int M);                   /* 1 if kernels are instantiated for M */
+/* Hermite bound C_{M+1}: max_hermite_root (tables.cpp:22-41, hermite.hpp:23-26) */
+double momg_max_hermite_root(int degree);
+
+/* ---- fields (CellField, grid.hpp:54-85) -------------------------------- */
+int momg_field_create(const momg_grid* grid, int M, momg_field** out, momg_err* err);
+void momg_field_destroy(momg_field* f);
+int momg_field_shape(const momg_field* f, int* nx, int* ny, int* M, int* N, int* NP);
+int momg_field_upload(momg_field* f, const double* coeffs, const double* params, momg_err* err);
+int momg_field_download(const momg_field* f, double* coeffs, double* params, momg_err* err);
+int momg_field_upload_async(momg_field* f, const double* coeffs, const double* params, momg_err* err);
+int momg_field_download_async(const momg_field* f, double* coeffs, double* params, momg_err* err);
+int momg_field_copy(momg_field* dst, const momg_field* src, momg_err* err);   /* CellField copy (multigrid.cpp:188) */
+int momg_field_fill_maxwellian(momg_field* f, double rho, const double u[3], double theta,
+                               momg_err* err);                               /* uniform_field (grid.hpp:79-85) */
+/* device pointers for zero-copy interop (coeffs [cells][NP], params [cells][4]) */
+int momg_field_device_ptrs(momg_field* f, double** coeffs, double** params);
+
+/* ---- the hot path ------------------------------------------------------ */
+/* residual (spatial.cpp:135-159): out <- R(field), out params <- field params */
+int momg_residual(const momg_ctx* ctx, const momg_field* field, momg_field* out, momg_err* err);
+/* fast_sweep_step (single_level.cpp:121-166): exact lexicographic Gauss-Seidel
+   order via anti-diagonal wavefronts; rhs nullable (empty RhsField);
+   sweep_order nullable ({0,1,2,3}); evals += cell updates (WorkStats) */
+int momg_fast_sweep(const momg_ctx* ctx, momg_field* field, const momg_field* rhs,
+                    const int* sweep_order, long long* evals, momg_err* err);
+/* euler_step (single_level.cpp:74-97) with residuals = R(field) evaluated inside */
+int momg_euler_step(const momg_ctx* ctx, momg_field* field, const momg_field* rhs, momg_err* err);
+/* total_mass / mass_correction (single_level.cpp:168-183) */
+int momg_total_mass(const momg_field* field, double* out, momg_err* err);
+int momg_mass_correction(momg_field* field, double target_mass, momg_err* err);
+/* restrict_solution (multigrid.cpp:67-112): coarse <- R_sol(fine) */
+int momg_restrict_solution(const momg_field* fine, momg_field* coarse, momg_err* err);
+/* restrict_residual (multigrid.cpp:114-142): out <- sum (a_c/S) project(arrays_c -> coarse basis) */
+int momg_restrict_residual(const momg_field* fine_arrays, const momg_field* coarse,
+                           momg_field* out, momg_err* err);
+/* fas_correct (multigrid.cpp:144-164) */
+int momg_fas_correct(momg_field* fine, const momg_field* coarse_before,
+                     const momg_field* coarse_after, momg_err* err);
+/* residual_norm (multigrid.cpp:202-218); theta from field params */
+int momg_residual_norm(const momg_field* res, const momg_field* field, double* out, momg_err* err);
+/* residual_scale (multigrid.cpp:224-239) */
+int momg_residual_scale(const momg_ctx* ctx, const momg_field* field, double* out, momg_err* err);
+/* defect of nmg_cycle (multigrid.cpp:178-185): out <- project(rhs -> res basis) - res,
+   or -res when rhs is null */
+int momg_defect(const momg_field* res, const momg_field* rhs, momg_field* out, momg_err* err);
+/* coarse_rhs += coarse_res (multigrid.cpp:192-193): dst.coeffs += src.coeffs */
+int momg_axpy(momg_field* dst, const momg_field* src, momg_err* err);
+
+/* ---- the host driver (kept as host C++, multigrid.cpp:44-65, 166-320) --- */
+/* nmg_cycle on the hierarchy GridHierarchy::build(field grid, levels) */
+int momg_nmg_cycle(const momg_ctx* ctx, momg_field* field, int levels, int s1, int s2, int s3,
+                   int gamma, long long* work, momg_err* err);
+/* solve_steady: NonConvergence -> MOMG_NONCONVERGENCE with the partial report */
+int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_opts* opts,
+                      momg_report* report, momg_err* err);
+
+/* ---- execution strategy of fast_sweep (same results either way) -------- */
+/* 1 (default): one persistent dataflow kernel per call; 0: one launch per
+   anti-diagonal (simple reference strategy).  Env MOMG_SWEEP=diag selects 0. */
+int momg_set_sweep_mode(int mode);
+
+/* ---- instrumentation --------------------------------------------------- */
+/* number of kernels this library has launched since load (gpu_launches) */
+long long momg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOMG_GPU_H */

@@ -1,0 +1,226 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle
+on identical seeded inputs.  Tolerances (north_star): per-sweep moment fields
+1e-10 relative (|d| <= 1e-10 max(1, |f0|), the idiom of
+test_projection.cpp:144-145); converged macroscopic fields 1e-8; NMG
+iteration counts within +-1."""
+import numpy as np
+import pytest
+
+from helpers import BGK, SHAKHOV, Ctx, Grid, Oracle, c5_field, cavity_ctx, smooth_field, uniform_field
+
+pytestmark = pytest.mark.gpu
+
+momg = pytest.importorskip("paper_2206_13164_b200.momg")
+O = Oracle("port")
+
+TOL = 1e-10
+
+
+def mctx(octx: Ctx) -> "momg.SolveContext":
+    """Same configuration as an oracle Ctx, as the product's SolveContext."""
+    W = momg.WallSpec
+    walls = momg.Walls(*(W(octx.wall_speed[k], octx.wall_theta[k]) for k in range(4)))
+    return momg.SolveContext(walls, momg.CollisionModel(momg.CollisionKind(octx.collision), octx.prandtl),
+                             momg.GasParams(octx.knudsen, octx.viscosity_index),
+                             momg.SpatialScheme(octx.space_order, octx.c_bound),
+                             momg.CflPolicy(octx.cfl, octx.c_bound if octx.cfl_c_bound is None else octx.cfl_c_bound))
+
+
+def mgrid(g: Grid) -> "momg.Grid2D":
+    return momg.Grid2D(g.nx, g.ny, g.Lx, g.Ly, g.dx.copy(), g.dy.copy(), g.xc.copy(), g.yc.copy())
+
+
+def rel_field(got, want):
+    scale = np.maximum(1.0, np.abs(want[:, :1]))
+    return float(np.max(np.abs(got - want) / scale))
+
+
+def rel_res(got, want):
+    scale = np.maximum(1.0, np.max(np.abs(want), axis=1, keepdims=True))
+    return float(np.max(np.abs(got - want) / scale))
+
+
+@pytest.fixture(params=["persistent", "diag"])
+def sweep_mode(request):
+    momg.set_sweep_mode(request.param)
+    yield request.param
+    momg.set_sweep_mode("persistent")
+
+
+CASES = [
+    # (M, order, model, nx, ny, uz)
+    (3, 1, BGK, 8, 6, False),
+    (3, 2, BGK, 9, 8, False),
+    (4, 1, SHAKHOV, 7, 7, True),
+    (5, 1, SHAKHOV, 7, 6, True),
+    (5, 2, BGK, 8, 8, False),
+    (6, 2, BGK, 6, 5, False),
+    (7, 1, BGK, 5, 6, True),
+    (8, 2, SHAKHOV, 6, 6, False),
+]
+
+
+def _setup(M, order, model, nx, ny, uz, seed=3):
+    g = Grid.uniform(nx, ny, 1.0, 1.1)
+    octx = cavity_ctx(M, order, model, kn=0.3, prandtl=2.0 / 3.0 if model == SHAKHOV else 1.0,
+                      bottom_theta=1.3)
+    c, p = smooth_field(g, M, seed=seed + 10 * M + nx, amp=0.08, uz=uz)
+    return g, octx, c, p
+
+
+@pytest.mark.parametrize("M,order,model,nx,ny,uz", CASES)
+def test_residual_parity(M, order, model, nx, ny, uz):
+    g, octx, c, p = _setup(M, order, model, nx, ny, uz)
+    want = O.residual(octx, g, c, p)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    got, gp = momg.residual(f, mctx(octx)).download()
+    assert rel_res(got, want) < TOL
+    np.testing.assert_array_equal(gp, p)  # residual params = cell params (spatial.cpp:128)
+
+
+@pytest.mark.parametrize("M,order,model,nx,ny,uz", CASES)
+def test_fast_sweep_parity(M, order, model, nx, ny, uz, sweep_mode):
+    g, octx, c, p = _setup(M, order, model, nx, ny, uz)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    ctx = mctx(octx)
+    wc, wp = c, p
+    for it in range(2):  # two consecutive FS iterations, each checked
+        wc, wp, ev = O.fast_sweep(octx, g, wc, wp)
+        work = momg.WorkStats()
+        momg.fast_sweep_step(f, None, ctx, work)
+        gc, gp = f.download()
+        assert work.cell_evals == ev == 4 * nx * ny
+        assert rel_field(gc, wc) < TOL, f"iteration {it}"
+        assert np.max(np.abs(gp - wp)) < TOL
+
+
+@pytest.mark.parametrize("order", [[2, 0, 3, 1], [1, 1, 3, 3]])
+def test_sweep_order_and_rhs(order, sweep_mode):
+    M = 5
+    g, octx, c, p = _setup(M, 2, BGK, 9, 7, False)
+    rc = c * 1e-3
+    rp = p.copy(); rp[:, 0] += 0.01; rp[:, 3] *= 1.02  # rhs in its own basis
+    wc, wp, _ = O.fast_sweep(octx, g, c, p, rhs=(rc, rp), sweep_order=order)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    rhs = momg.CellField.from_host(mgrid(g), M, rc, rp)
+    momg.fast_sweep_step(f, rhs, mctx(octx), None, tuple(order))
+    gc, gp = f.download()
+    assert rel_field(gc, wc) < TOL
+    assert np.max(np.abs(gp - wp)) < TOL
+
+
+@pytest.mark.parametrize("M", [3, 5, 6, 8])
+def test_transfer_operators_parity(M):
+    fg = Grid.uniform(8, 12, 1.0, 1.0)
+    cg = fg.coarsen()
+    c, p = smooth_field(fg, M, seed=11 + M, amp=0.1, uz=True)
+    wc, wp = O.restrict_solution(M, fg, c, p, cg)
+    fine = momg.CellField.from_host(mgrid(fg), M, c, p)
+    coarse = momg.restrict_solution(fine, mgrid(cg))
+    gc, gp = coarse.download()
+    assert rel_field(gc, wc) < TOL and np.max(np.abs(gp - wp)) < TOL
+    # restrict_residual of a defect carrying its own basis
+    octx = cavity_ctx(M, 1, BGK)
+    res = O.residual(octx, fg, c, p)
+    dp = p.copy(); dp[:, 1] += 0.02
+    want = O.restrict_residual(M, fg, -res, dp, p, cg, wp)
+    arrays = momg.CellField.from_host(mgrid(fg), M, -res, dp)
+    got, gpp = momg.restrict_residual(arrays, fine, coarse).download()
+    assert rel_res(got, want) < TOL
+    np.testing.assert_array_equal(gpp, gp)
+    # fas_correct
+    after = wc.copy(); after[:, 4:] += 1e-4 * np.sin(np.arange(after[:, 4:].size)).reshape(after[:, 4:].shape)
+    ap = wp.copy(); ap[:, 0] += 1e-3
+    want_c, want_p = O.fas_correct(M, fg, c, p, cg, wc, wp, after, ap)
+    before_f = momg.CellField.from_host(mgrid(cg), M, wc, wp)
+    after_f = momg.CellField.from_host(mgrid(cg), M, after, ap)
+    momg.fas_correct(fine, before_f, after_f)
+    gc2, gp2 = fine.download()
+    assert rel_field(gc2, want_c) < TOL and np.max(np.abs(gp2 - want_p)) < TOL
+
+
+def test_mass_and_norms_parity():
+    M = 5
+    g = Grid.uniform(33, 17, 1.3, 0.7)
+    c, p = c5_field(g.nx, g.ny, M, seed=5)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    assert abs(momg.total_mass(f) - O.total_mass(g, M, c)) <= 1e-14 * abs(O.total_mass(g, M, c))
+    momg.mass_correction(f, 0.77)
+    gc, _ = f.download()
+    assert rel_field(gc, O.mass_correction(g, M, c, 0.77)) < 1e-14
+    octx = cavity_ctx(M, 1, BGK)
+    res = O.residual(octx, g, c, p)
+    rf = momg.CellField.from_host(mgrid(g), M, res, p)
+    f2 = momg.CellField.from_host(mgrid(g), M, c, p)
+    want = O.residual_norm(M, g, res, p)
+    assert abs(momg.residual_norm(rf, f2) - want) <= 1e-13 * want
+
+
+def test_nmg_cycle_parity():
+    M = 3
+    g = Grid.uniform(16, 16)
+    octx = cavity_ctx(M, 1, BGK, kn=0.1, lid=0.1)
+    c, p = uniform_field(g, M)
+    wc, wp, ww = O.nmg_cycle(octx, g, c, p, levels=2)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    work = momg.WorkStats()
+    momg.nmg_cycle(f, mctx(octx), levels=2, work=work)
+    gc, gp = f.download()
+    assert work.cell_evals == ww
+    assert rel_field(gc, wc) < TOL and np.max(np.abs(gp - wp)) < TOL
+
+
+def macro(c, p):
+    """rho, u, theta, heat flux, stress of Grad-normalized cells (extract_macro)."""
+    rho = c[:, 0]
+    q = np.stack([3 * c[:, 10] + c[:, 13] + c[:, 15], 3 * c[:, 16] + c[:, 11] + c[:, 18],
+                  3 * c[:, 19] + c[:, 12] + c[:, 17]], axis=1)
+    sig = np.stack([2 * c[:, 4], c[:, 5], c[:, 6], 2 * c[:, 7], c[:, 8], 2 * c[:, 9]], axis=1)
+    return np.concatenate([rho[:, None], p, q, sig], axis=1)
+
+
+@pytest.mark.parametrize("solver,nx,levels", [("nmg", 16, 2), ("fs", 16, 0), ("nmg", 32, 0)])
+def test_solve_steady_parity(solver, nx, levels):
+    """Converged macroscopic fields within 1e-8 and iteration counts within +-1
+    (acceptance-style cavity, M = 3, first order)."""
+    M = 3
+    g = Grid.uniform(nx, nx)
+    octx = cavity_ctx(M, 1, BGK, kn=0.1, lid=0.1)
+    c, p = uniform_field(g, M)
+    kind = {"fs": 1, "nmg": 2}[solver]
+    wc, wp, wr = O.solve_steady(octx, g, c, p, solver=kind, tol=1e-8, levels=levels)
+    assert wr["converged"]
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    opts = momg.SolverOptions(momg.SolverKind(kind), 1e-8, 0, levels)
+    rep = momg.solve_steady(f, mctx(octx), opts)
+    assert rep.converged
+    assert abs(rep.iterations - wr["iterations"]) <= 1
+    gc, gp = f.download()
+    mg, mw = macro(gc, gp), macro(wc, wp)
+    assert np.max(np.abs(mg - mw)) <= 1e-8 * np.max(np.abs(mw))
+
+
+def test_dt_halving_and_solver_error(sweep_mode):
+    """test_single_level.cpp:135-156 on the device: the first visit survives
+    only at dt/2 (rho = 1 - 0.5*0.045*30), the second raises SolverError and
+    leaves the cell in its pre-update state."""
+    g = momg.Grid2D.uniform(1, 1, 0.1, 0.1)
+    ctx = momg.SolveContext(scheme=momg.SpatialScheme(1, 1.0), cfl=momg.CflPolicy(0.9, 1.0),
+                            gas=momg.GasParams(1e300))
+    f = momg.uniform_field(g, 3, 1.0, (0.0, 0.0, 0.0), 1.0)
+    rc = np.zeros((1, 20)); rc[0, 0] = 30.0
+    rhs = momg.CellField.from_host(g, 3, rc, np.array([[0, 0, 0, 1.0]]))
+    with pytest.raises(momg.SolverError):
+        momg.fast_sweep_step(f, rhs, ctx)
+    c, _ = f.download()
+    assert c[0, 0] == pytest.approx(1.0 - 0.5 * 0.045 * 30.0, rel=1e-12)
+
+
+def test_nonconvergence_carries_report():
+    M = 3
+    g = momg.Grid2D.uniform(16, 16)
+    ctx = momg.cavity_context(M, 1)
+    f = momg.uniform_field(g, M, 1.0, (0, 0, 0), 1.0)
+    with pytest.raises(momg.NonConvergence) as ei:
+        momg.solve_steady(f, ctx, momg.SolverOptions(momg.SolverKind.fs, 1e-8, 3))
+    assert ei.value.report.iterations == 3 and len(ei.value.report.history) == 3
