@@ -1,0 +1,381 @@
+"""Benchmark of the B200 NMG / fast-sweeping hot path (BASELINE.json metric:
+smoother cell-updates/s (FP64) + NMG wall time to residual 1e-8).
+
+Workload (BASELINE.json configs[4], "C5"): 2048x2048 cells, M = 5 (56
+moments/cell), FP64, seeded random field (rho~U[0.9,1.1], u_x,u_y~N(0,0.05),
+u_z=0, theta~U[0.9,1.1], f_alpha~N(0,1e-3)*0.5^|alpha|), diffuse walls at
+theta = 1, BGK Kn = 0.1, first-order FV.  One step = one full four-direction
+fast-sweeping iteration (the exact-order dataflow kernel) + one residual + one
+restrict/prolong pair (restrict_solution, restrict_residual of the defect,
+fas_correct with after = before + seeded delta).  value = 4*nx*ny smoother
+cell updates / step time (residual and transfer time included).
+
+Default run also reports NMG time-to-1e-8 on C2 (128^2, M = 5, second order,
+NMG over 4 levels) as "nmg".  --impl reference times the reference's own CPU
+implementation (oracle/_ref: /root/reference compiled against the shims,
+OpenMP blocked FS with every host thread) on a bounded sample of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+FLOPS_PER_UPDATE_C5 = 16290.0  # M=5, order 1, 3-axis shifts (C5)
+BYTES_PER_UPDATE_C5 = 960.0    # 2*(N+4)*8 minimum HBM bytes per cell update
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=2048)
+    ap.add_argument("--M", type=int, default=5)
+    ap.add_argument("--order", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=2206)
+    ap.add_argument("--no-nmg", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=96)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.path = f"/tmp/momg_clocks_{os.getpid()}.csv"
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx = max(mx, float(f[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except OSError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["fp64_tflops"], "measured DFMA probe (profiles/fp64_peak.json, tools/fp64_peak.cu)"
+    return 37.0, "nominal B200 FP64 (unmeasured fallback)"
+
+
+# --------------------------------------------------------------- CPU legs
+def cpu_sample_rate(kind: str, nx: int, M: int, order: int, threads: int, seed: int,
+                    steps: int = 1):
+    """Cell-updates/s of the CPU implementation on an nx x nx sample of the
+    C5 workload (FS + residual + restrict pair per step, like the GPU step)."""
+    from oracle.api import BGK, Ctx, Grid, Oracle
+    from paper_2206_13164_b200.synthetic import c5_field
+
+    o = Oracle(kind)
+    g = Grid.uniform(nx, nx)
+    cg = g.coarsen()
+    cb = o.max_hermite_root(M + 1)
+    ctx = Ctx(M=M, space_order=order, c_bound=cb, cfl=0.9, cfl_c_bound=cb, collision=BGK,
+              knudsen=0.1, threads=threads)
+    c, p = c5_field(nx, nx, M, seed=seed)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        c, p, _ = o.fast_sweep(ctx, g, c, p)
+        res = o.residual(ctx, g, c, p)
+        cc, cp = o.restrict_solution(M, g, c, p, cg)
+        o.restrict_residual(M, g, -res, p, p, cg, cp)
+        after = cc.copy()
+        after[:, 10:] += 1e-6
+        c, p = o.fas_correct(M, g, c, p, cg, cc, cp, after, cp)
+    dt = time.perf_counter() - t0
+    return 4.0 * nx * nx * steps / dt, dt
+
+
+def reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    metric = "smoother cell-updates/s (FP64)"
+    nx = 128
+    from oracle.api import REF_LIB
+    if not os.path.exists(REF_LIB):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libmomg_ref.so not built (needs /root/reference)"}))
+        return
+    rates = []
+    for s in range(a.warmup + a.steps):
+        r, dt = cpu_sample_rate("reference", nx, a.M, a.order, threads, a.seed + s)
+        if s >= a.warmup:
+            rates.append((r, dt))
+    value = statistics.median(r for r, _ in rates)
+    ms = 1e3 * 4 * a.nx * a.nx / value
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": "cell-updates/s",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"C5 sample {nx}x{nx} of {a.nx}x{a.nx}, M={a.M}, order {a.order}",
+                       "fs": "reference OpenMP blocked fast_sweep_step (threads=%d, non-exact order)" % threads},
+            "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{nx}x{nx} C5 sub-field, 1 FS + residual + restrict pair per step"},
+            "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------- GPU arm
+def ours(a):
+    import torch
+
+    from paper_2206_13164_b200 import momg
+    from paper_2206_13164_b200.synthetic import c5_field
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    err = momg._Err()
+    momg.lib().momg_init(local, momg.C.byref(err))
+    momg.lib().momg_set_stream(momg.C.c_void_p(stream.cuda_stream))
+
+    nx, M = a.nx, a.M
+    N = momg.count(M)
+    g = momg.Grid2D.uniform(nx, nx)
+    cgrid = momg.Grid2D(nx // 2, nx // 2, 1.0, 1.0, *_coarse_arrays(g))
+    ctx = momg.cavity_context(M, a.order, knudsen=0.1, lid=0.0)
+    c_host, p_host = c5_field(nx, nx, M, seed=a.seed + rank)
+    f = momg.CellField.from_host(g, M, c_host, p_host)
+    res = momg.CellField(g, M)
+    coarse = momg.CellField(cgrid, M)
+    before = momg.CellField(cgrid, M)
+    after = momg.CellField(cgrid, M)
+    crhs = momg.CellField(cgrid, M)
+    dc, _ = c5_field(nx // 2, nx // 2, M, seed=a.seed + 99)
+    dc[:, :10] = 0.0
+    dc *= 1e-3
+    delta = momg.CellField.from_host(cgrid, M, dc, np.zeros((cgrid.cells(), 4)))
+    L = momg.lib()
+    E = momg._Err
+    C = momg.C
+
+    def step(evs=None):
+        e = E()
+        if evs:
+            evs[0].record(stream)
+        momg.fast_sweep_step(f, None, ctx)
+        if evs:
+            evs[1].record(stream)
+        c = ctx._c(M)
+        L.momg_residual(C.byref(c), f.handle, res.handle, C.byref(e))
+        if evs:
+            evs[2].record(stream)
+        L.momg_restrict_solution(f.handle, coarse.handle, C.byref(e))
+        L.momg_field_copy(before.handle, coarse.handle, C.byref(e))
+        L.momg_defect(res.handle, None, res.handle, C.byref(e))
+        L.momg_restrict_residual(res.handle, coarse.handle, crhs.handle, C.byref(e))
+        L.momg_field_copy(after.handle, coarse.handle, C.byref(e))
+        L.momg_axpy(after.handle, delta.handle, C.byref(e))
+        L.momg_fas_correct(f.handle, before.handle, after.handle, C.byref(e))
+        if evs:
+            evs[3].record(stream)
+        if e.code:
+            raise RuntimeError(e.msg.decode())
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
+    launches0 = momg.launch_count()
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for s in range(a.steps):
+            step(evs[s])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    launches = momg.launch_count() - launches0
+    total_ms = t0.elapsed_time(t1)
+    if dist:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / a.steps
+    sweep_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    resid_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    xfer_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    updates = 4.0 * nx * nx
+    value = updates * world / (ms_step * 1e-3)
+
+    # ---- end to end through the C ABI: host (pinned) -> device -> step -> host
+    e2e = None
+    if not a.no_e2e:
+        hc = torch.empty((nx * nx, N), dtype=torch.float64, pin_memory=True).numpy()
+        hp = torch.empty((nx * nx, 4), dtype=torch.float64, pin_memory=True).numpy()
+        hc[:] = c_host
+        hp[:] = p_host
+        oc = torch.empty((nx * nx, N), dtype=torch.float64, pin_memory=True).numpy()
+        op = torch.empty((nx * nx, 4), dtype=torch.float64, pin_memory=True).numpy()
+        ec = momg._dp(hc); ep = momg._dp(hp); eoc = momg._dp(oc); eop = momg._dp(op)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            e = E()
+            L.momg_field_upload_async(f.handle, ec, ep, C.byref(e))
+            step()
+            L.momg_field_download_async(f.handle, eoc, eop, C.byref(e))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / a.steps
+        if dist:
+            tt = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        assert np.isfinite(oc[:, 0]).all()
+        nbytes = hc.nbytes + hp.nbytes
+        e2e = {"value": updates * world / (e2e_ms * 1e-3), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": oc.nbytes + op.nbytes,
+               "ms_per_step": e2e_ms}
+
+    # ---- NMG time-to-1e-8 on C2 (128^2, M=5, order 2, 4 levels)
+    nmg = None
+    if not a.no_nmg and rank == 0:
+        nmg = run_nmg_c2(momg)
+
+    # ---- roofline of the dominant kernel (persistent FS sweep)
+    peak, peak_src = fp64_peak()
+    sweep_med = statistics.median(sweep_ms)
+    achieved = FLOPS_PER_UPDATE_C5 * updates / (sweep_med * 1e-3) / 1e12
+    roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": None, "kernel": "k_sweep_persistent<5>",
+            "flops_per_update": FLOPS_PER_UPDATE_C5, "peak_source": peak_src,
+            "kernel_ms": sweep_med,
+            "note": "FP64 CUDA cores (no tensor-core path); hbm bytes/update >= 960, AI ~17 flop/B"}
+
+    cpu = None
+    if not a.no_cpu and rank == 0 and world == 1:
+        r, dt = cpu_sample_rate("port", a.cpu_sample, M, a.order, 1, a.seed)
+        cpu = {"value": r, "unit": "cell-updates/s", "cores": 1, "kind": "port",
+               "sample": f"{a.cpu_sample}x{a.cpu_sample} C5 sub-field, 1 FS + residual + restrict pair "
+                         f"({dt:.1f} s, C restatement oracle/momg_oracle.c, 1 thread)"}
+
+    if rank == 0:
+        line = {"metric": "smoother cell-updates/s (FP64)", "value": value, "unit": "cell-updates/s",
+                "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"C5: {nx}x{nx}, M={M} ({N} moments), order {a.order}, BGK Kn 0.1, "
+                                       "walls theta=1; step = FS iteration + residual + restrict/prolong pair",
+                           "global_cells": nx * nx * world, "parallelism": f"replicas x{world}",
+                           "l2": "inputs larger than L2 (field %.2f GB)" % (nx * nx * (N + 4) * 8 / 1e9),
+                           "sweep": "persistent dataflow, exact lexicographic GS order"},
+                "breakdown_ms": {"fast_sweep": sweep_med, "residual": statistics.median(resid_ms),
+                                 "restrict_prolong": statistics.median(xfer_ms)},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "nmg": nmg}
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def _coarse_arrays(g):
+    nx, ny = g.nx // 2, g.ny // 2
+    dx = g.dx[0::2] + g.dx[1::2]
+    dy = g.dy[0::2] + g.dy[1::2]
+    xc = np.cumsum(dx) - 0.5 * dx
+    yc = np.cumsum(dy) - 0.5 * dy
+    return dx, dy, xc, yc
+
+
+def run_nmg_c2(momg):
+    """C2: 128x128 lid cavity, Kn 0.1, M = 5, second order, NMG over 4 levels,
+    uniform Maxwellian start, until ||R||/||R0|| <= 1e-8 (multigrid.cpp:243-320)."""
+    import torch
+    g = momg.Grid2D.uniform(128, 128)
+    ctx = momg.cavity_context(5, 2, knudsen=0.1, lid=0.1)
+    f = momg.uniform_field(g, 5, 1.0, (0.0, 0.0, 0.0), 1.0)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    try:
+        rep = momg.solve_steady(f, ctx, momg.SolverOptions(momg.SolverKind.nmg, 1e-8, 0, 4))
+        ok = True
+    except momg.NonConvergence as e:
+        rep, ok = e.report, False
+    wall = time.perf_counter() - t
+    return {"config": "C2 128x128 M=5 order 2 BGK Kn 0.1 NMG levels 4 (V(2,2), s3=4)",
+            "seconds": wall, "converged": ok, "iterations": rep.iterations,
+            "final_ratio": rep.final_ratio, "work_cell_updates": rep.work}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        reference_arm(a)
+    else:
+        ours(a)
+
+
+if __name__ == "__main__":
+    main()
