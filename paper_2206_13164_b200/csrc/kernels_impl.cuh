@@ -3,8 +3,8 @@
 //
 //   K1 k_residual        residual()            spatial.cpp:135-159
 //   K2 k_sweep_diag      fast_sweep_step()     single_level.cpp:121-166
-//      (one anti-diagonal of one sweep direction per launch; see also the
-//       persistent dataflow sweep in sweep_persistent.cuh)
+//      (one anti-diagonal per launch; the default is the persistent dataflow
+//       sweep of sweep_persistent.cuh)
 //   K3 k_restrict_sol    restrict_solution()   multigrid.cpp:67-112
 //      k_restrict_res    restrict_residual()   multigrid.cpp:114-142
 //   K4 k_fas_correct     fas_correct()         multigrid.cpp:144-164
@@ -19,30 +19,33 @@
 #include "momg_cell.cuh"
 #include "runtime.h"
 #include "sweep_persistent.cuh"
+#include "kernels_v3.cuh"
 
 namespace momg_gpu {
 
 constexpr int WPB = 4;  // warps per block for the per-cell kernels
 
 // ------------------------------------------------------------------- K1
-template <int M>
+template <int M, int ORDER>
 __global__ void __launch_bounds__(WPB * 32) k_residual(DevField f, DevField out, DevCtx ctx,
                                                        DevErr* err) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const BlockView bv = block_setup<M>(smem_raw, &ctx, &f, &out, nullptr, nullptr);
-  WarpBuf<M>& sb = warp_buf<M>(bv);
+  const BlockView bv = block_setup<M, ORDER>(smem_raw, &ctx, &f, &out, nullptr, nullptr);
+  WarpBuf<M, ORDER>& sb = warp_buf<M, ORDER>(bv);
   const DevField* F = &bv.hdr->f;
   const int cells = f.nx * f.ny;
   for (int cell = blockIdx.x * WPB + (threadIdx.x >> 5); cell < cells; cell += gridDim.x * WPB) {
     if (err_set(err)) return;
     const int i = cell % f.nx, j = cell / f.nx;
-    load_cell<M>(F, cell, sb.S, sb.cp);
-    const int w = cell_residual_smem<M>(F, &bv.hdr->ctx, bv.alpha, i, j, sb.cp, sb);
+    load_stencil<M, ORDER>(F, i, j, sb);
+    double R[Cfg<M>::T];
+    const int w = cell_residual<M, ORDER>(F, &bv.hdr->ctx, bv.tab, i, j, sb, R);
     if (w) {
       if (lane_id() == 0) raise_err(err, code_of(w), w, i, j, 0.0);
       return;
     }
-    store_cell<M>(&bv.hdr->g, cell, sb.R, sb.cp);
+    store_cell_regs<M>(&bv.hdr->g, cell, R, sb.cp[0]);
+    __syncwarp();
   }
 }
 
@@ -51,22 +54,23 @@ __global__ void __launch_bounds__(WPB * 32) k_residual(DevField f, DevField out,
 // ii + jj = d, ii = i_up ? i : nx-1-i, jj = j_up ? j : ny-1-j.  Cells on one
 // anti-diagonal are independent (cross stencil), so successive launches give
 // exactly the lexicographic Gauss-Seidel order of single_level.cpp:146-153.
-template <int M>
+template <int M, int ORDER>
 __global__ void __launch_bounds__(WPB * 32) k_sweep_diag(DevField f, DevField rhs, int has_rhs,
                                                          DevCtx ctx, DevErr* err, int i_up,
                                                          int j_up, int d, int ii0, int count) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (err_set(err)) return;
-  const BlockView bv = block_setup<M>(smem_raw, &ctx, &f, &rhs, nullptr, nullptr);
+  const BlockView bv = block_setup<M, ORDER>(smem_raw, &ctx, &f, &rhs, nullptr, nullptr);
   const int q = blockIdx.x * WPB + (threadIdx.x >> 5);
   if (q >= count) return;
-  WarpBuf<M>& sb = warp_buf<M>(bv);
+  WarpBuf<M, ORDER>& sb = warp_buf<M, ORDER>(bv);
   const int ii = ii0 + q, jj = d - ii;
   const int i = i_up ? ii : f.nx - 1 - ii;
   const int j = j_up ? jj : f.ny - 1 - jj;
   double bad = 0.0;
-  const int w = sweep_cell_smem<M>(&bv.hdr->f, has_rhs ? &bv.hdr->g : nullptr, &bv.hdr->ctx,
-                                   bv.alpha, i, j, sb, &bad);
+  load_stencil<M, ORDER>(&bv.hdr->f, i, j, sb);
+  const int w = sweep_cell<M, ORDER>(&bv.hdr->f, has_rhs ? &bv.hdr->g : nullptr, &bv.hdr->ctx,
+                                     bv.tab, i, j, sb, &bad);
   if (w && lane_id() == 0) raise_err(err, code_of(w), w, i, j, bad);
 }
 
@@ -75,26 +79,28 @@ template <int M>
 __global__ void __launch_bounds__(WPB * 32) k_restrict_sol(DevField fine, DevField coarse,
                                                            DevErr* err) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const BlockView bv = block_setup<M>(smem_raw, nullptr, &fine, &coarse, nullptr, nullptr);
-  WarpBuf<M>& sb = warp_buf<M>(bv);
-  const DevField* Fi = &bv.hdr->f;
+  const BlockView bv = block_setup<M, 1>(smem_raw, nullptr, &fine, &coarse, nullptr, nullptr);
+  WarpBuf<M, 1>& sb = warp_buf<M, 1>(bv);
+  constexpr int T = Cfg<M>::T;
   const int lane = lane_id();
   const int cells = coarse.nx * coarse.ny;
   for (int K = blockIdx.x * WPB + (threadIdx.x >> 5); K < cells; K += gridDim.x * WPB) {
     if (err_set(err)) return;
     const int I = K % coarse.nx, J = K / coarse.nx;
-    size_t child[4];
     double area[4];
-    double S = 0.0, mass = 0.0, energy = 0.0, mom[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int i = 2 * I + c % 2, j = 2 * J + c / 2;
-      child[c] = (size_t)j * fine.nx + i;
       area[c] = fine.dx[i] * fine.dy[j];
-      const double rho = ldg_cg(fine.c + child[c] * Cfg<M>::NP);
-      double u[4];
+      load_cell_async<M>(&bv.hdr->f, (size_t)j * fine.nx + i, sb.cell[c], sb.cp[c]);
+    }
+    __syncwarp();
+    // conservation of mass, momentum, energy over the children (multigrid.cpp:83-93)
+    double S = 0.0, mass = 0.0, energy = 0.0, mom[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) u[q] = ldg_cg(fine.p + child[c] * 4 + q);
+    for (int c = 0; c < 4; ++c) {
+      const double rho = sb.cell[c][0];
+      const double* u = sb.cp[c];
       S += area[c];
       mass += rho * area[c];
 #pragma unroll
@@ -112,23 +118,31 @@ __global__ void __launch_bounds__(WPB * 32) k_restrict_sol(DevField fine, DevFie
       if (lane == 0) raise_err(err, E_NONPHYSICAL, W_RESTRICT, I, J, rho_H);
       return;
     }
-    for (int k = lane; k < Cfg<M>::N; k += 32) sb.R[k] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) proj_coeffs<M>(p4(sb.cp[c]), basis, sb.c[c]);
+    __syncwarp();
+    double acc[T], v[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[t] = 0.0;
     for (int c = 0; c < 4; ++c) {
-      load_cell<M>(Fi, child[c], sb.A, sb.par);
-      project_smem<M>(bv.alpha, sb.A, sb.A2, p4(sb.par), basis, sb.A);
+      project_apply<M>(bv.tab, sb.cell[c], sb.X1, sb.X2, sb.c[c], pass_mask(p4(sb.cp[c]), basis), v);
       const double wgt = area[c] / S;
-      for (int k = lane; k < Cfg<M>::N; k += 32) sb.R[k] = fma(wgt, sb.A[k], sb.R[k]);
-      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t] = fma(wgt, v[t], acc[t]);
     }
-    if (lane < 4) sb.cp[lane] = basis.v[lane];
+    __syncwarp();
+    store_items<M>(sb.LA, acc);
+    if (lane < 4) sb.par[lane] = basis.v[lane];
     __syncwarp();
     double bad = 0.0;
-    const int w = grad_normalize_smem<M>(bv.alpha, sb.R, sb.A2, sb.cp, &bad);
+    const double* res;
+    const int w = grad_normalize<M, 1>(bv.tab, sb, sb.LA, sb.X1, sb.X2, sb.par, acc, &bad, &res);
     if (w) {
       if (lane == 0) raise_err(err, code_of(w), w, I, J, bad);
       return;
     }
-    store_cell<M>(&bv.hdr->g, K, sb.R, sb.cp);
+    store_cell_regs<M>(&bv.hdr->g, K, acc, sb.par);
+    __syncwarp();
   }
 }
 
@@ -136,8 +150,9 @@ template <int M>
 __global__ void __launch_bounds__(WPB * 32) k_restrict_res(DevField arrays, DevField coarse,
                                                            DevField out, DevErr* err) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const BlockView bv = block_setup<M>(smem_raw, nullptr, &arrays, &coarse, &out, nullptr);
-  WarpBuf<M>& sb = warp_buf<M>(bv);
+  const BlockView bv = block_setup<M, 1>(smem_raw, nullptr, &arrays, &coarse, &out, nullptr);
+  WarpBuf<M, 1>& sb = warp_buf<M, 1>(bv);
+  constexpr int T = Cfg<M>::T;
   const int lane = lane_id();
   const int cells = coarse.nx * coarse.ny;
   for (int K = blockIdx.x * WPB + (threadIdx.x >> 5); K < cells; K += gridDim.x * WPB) {
@@ -151,22 +166,28 @@ __global__ void __launch_bounds__(WPB * 32) k_restrict_res(DevField arrays, DevF
     for (int c = 0; c < 4; ++c) {
       const int i = 2 * I + c % 2, j = 2 * J + c / 2;
       S += arrays.dx[i] * arrays.dy[j];
+      load_cell_async<M>(&bv.hdr->f, (size_t)j * arrays.nx + i, sb.cell[c], sb.cp[c]);
     }
-    for (int k = lane; k < Cfg<M>::N; k += 32) sb.R[k] = 0.0;
+    __syncwarp();
+    if (!(basis.v[3] > 0.0)) {
+      if (lane == 0) raise_err(err, E_NONPHYSICAL, W_PROJ_SPREAD, I, J, basis.v[3]);
+      return;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) proj_coeffs<M>(p4(sb.cp[c]), basis, sb.c[c]);
+    __syncwarp();
+    double acc[T], v[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[t] = 0.0;
     for (int c = 0; c < 4; ++c) {
       const int i = 2 * I + c % 2, j = 2 * J + c / 2;
-      load_cell<M>(&bv.hdr->f, (size_t)j * arrays.nx + i, sb.A, sb.par);
-      if (!project_smem<M>(bv.alpha, sb.A, sb.A2, p4(sb.par), basis, sb.A)) {
-        if (lane == 0) raise_err(err, E_NONPHYSICAL, W_PROJ_SPREAD, I, J, basis.v[3]);
-        return;
-      }
+      project_apply<M>(bv.tab, sb.cell[c], sb.X1, sb.X2, sb.c[c], pass_mask(p4(sb.cp[c]), basis), v);
       const double wgt = (arrays.dx[i] * arrays.dy[j]) / S;
-      for (int k = lane; k < Cfg<M>::N; k += 32) sb.R[k] = fma(wgt, sb.A[k], sb.R[k]);
-      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t] = fma(wgt, v[t], acc[t]);
     }
-    if (lane < 4) sb.cp[lane] = basis.v[lane];
+    store_cell_regs<M>(&bv.hdr->h, K, acc, basis.v);
     __syncwarp();
-    store_cell<M>(&bv.hdr->h, K, sb.R, sb.cp);
   }
 }
 
@@ -175,32 +196,48 @@ template <int M>
 __global__ void __launch_bounds__(WPB * 32) k_fas_correct(DevField fine, DevField before,
                                                           DevField after, DevErr* err) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const BlockView bv = block_setup<M>(smem_raw, nullptr, &fine, &before, &after, nullptr);
-  WarpBuf<M>& sb = warp_buf<M>(bv);
+  const BlockView bv = block_setup<M, 1>(smem_raw, nullptr, &fine, &before, &after, nullptr);
+  WarpBuf<M, 1>& sb = warp_buf<M, 1>(bv);
+  constexpr int T = Cfg<M>::T;
   const int lane = lane_id();
   const int cells = fine.nx * fine.ny;
   for (int k = blockIdx.x * WPB + (threadIdx.x >> 5); k < cells; k += gridDim.x * WPB) {
     if (err_set(err)) return;
     const int i = k % fine.nx, j = k / fine.nx;
     const size_t K = (size_t)(j / 2) * before.nx + (i / 2);
-    load_cell<M>(&bv.hdr->f, k, sb.S, sb.cp);
-    load_cell<M>(&bv.hdr->h, K, sb.A, sb.par);
-    load_cell<M>(&bv.hdr->g, K, sb.B, sb.par + 4);
-    if (!project_smem<M>(bv.alpha, sb.A, sb.A2, p4(sb.par), p4(sb.cp), sb.A) ||
-        !project_smem<M>(bv.alpha, sb.B, sb.B2, p4(sb.par + 4), p4(sb.cp), sb.B)) {
-      if (lane == 0) raise_err(err, E_NONPHYSICAL, W_PROJ_SPREAD, i, j, sb.cp[3]);
+    load_cell_async<M>(&bv.hdr->f, k, sb.cell[0], sb.cp[0]);
+    load_cell_async<M>(&bv.hdr->h, K, sb.cell[1], sb.cp[1]);
+    load_cell_async<M>(&bv.hdr->g, K, sb.cell[2], sb.cp[2]);
+    __syncwarp();
+    const P4 cp = p4(sb.cp[0]), ap = p4(sb.cp[1]), bp = p4(sb.cp[2]);
+    if (!(cp.v[3] > 0.0)) {
+      if (lane == 0) raise_err(err, E_NONPHYSICAL, W_PROJ_SPREAD, i, j, cp.v[3]);
       return;
     }
-    for (int q = lane; q < Cfg<M>::N; q += 32) sb.S[q] += sb.A[q] - sb.B[q];
+    proj_coeffs<M>(ap, cp, sb.c[0]);
+    proj_coeffs<M>(bp, cp, sb.c[1]);
+    __syncwarp();
+    double va[T], vb[T];
+    const double *pa, *pb;
+    project_apply2<M>(bv.tab, sb.cell[1], sb.X1, sb.X2, sb.c[0], pass_mask(ap, cp), va,
+                      sb.cell[2], sb.Y1, sb.Y2, sb.c[1], pass_mask(bp, cp), vb, &pa, &pb);
+    double v[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) v[t] = sb.cell[0][item_pos<M>(t)] + (va[t] - vb[t]);
+    __syncwarp();
+    store_items<M>(sb.LA, v);
+    if (lane < 4) sb.par[lane] = cp.v[lane];
     __syncwarp();
     double bad = 0.0;
-    int w = grad_normalize_smem<M>(bv.alpha, sb.S, sb.A2, sb.cp, &bad);
+    const double* res;
+    int w = grad_normalize<M, 1>(bv.tab, sb, sb.LA, sb.X1, sb.X2, sb.par, v, &bad, &res);
     if (w) {
       if (code_of(w) == E_NONPHYSICAL) w = W_FAS;
       if (lane == 0) raise_err(err, code_of(w), w, i, j, bad);
       return;
     }
-    store_cell<M>(&bv.hdr->f, k, sb.S, sb.cp);
+    store_cell_regs<M>(&bv.hdr->f, k, v, sb.par);
+    __syncwarp();
   }
 }
 
@@ -209,25 +246,34 @@ template <int M>
 __global__ void __launch_bounds__(WPB * 32) k_defect(DevField res, DevField rhs, int has_rhs,
                                                      DevField out, DevErr* err) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const BlockView bv = block_setup<M>(smem_raw, nullptr, &res, &rhs, &out, nullptr);
-  WarpBuf<M>& sb = warp_buf<M>(bv);
+  const BlockView bv = block_setup<M, 1>(smem_raw, nullptr, &res, &rhs, &out, nullptr);
+  WarpBuf<M, 1>& sb = warp_buf<M, 1>(bv);
+  constexpr int T = Cfg<M>::T;
   const int lane = lane_id();
   const int cells = res.nx * res.ny;
   for (int k = blockIdx.x * WPB + (threadIdx.x >> 5); k < cells; k += gridDim.x * WPB) {
     if (err_set(err)) return;
-    load_cell<M>(&bv.hdr->f, k, sb.S, sb.cp);
+    load_cell_async<M>(&bv.hdr->f, k, sb.cell[0], sb.cp[0]);
+    if (has_rhs) load_cell_async<M>(&bv.hdr->g, k, sb.cell[1], sb.cp[1]);
+    __syncwarp();
+    double v[T];
     if (!has_rhs) {
-      for (int q = lane; q < Cfg<M>::N; q += 32) sb.R[q] = -sb.S[q];
+#pragma unroll
+      for (int t = 0; t < T; ++t) v[t] = -sb.cell[0][item_pos<M>(t)];
     } else {
-      load_cell<M>(&bv.hdr->g, k, sb.A, sb.par);
-      if (!project_smem<M>(bv.alpha, sb.A, sb.A2, p4(sb.par), p4(sb.cp), sb.A)) {
-        if (lane == 0) raise_err(err, E_NONPHYSICAL, W_PROJ_SPREAD, k % res.nx, k / res.nx, sb.cp[3]);
+      const P4 rp = p4(sb.cp[0]), hp = p4(sb.cp[1]);
+      if (!(rp.v[3] > 0.0)) {
+        if (lane == 0) raise_err(err, E_NONPHYSICAL, W_PROJ_SPREAD, k % res.nx, k / res.nx, rp.v[3]);
         return;
       }
-      for (int q = lane; q < Cfg<M>::N; q += 32) sb.R[q] = sb.A[q] - sb.S[q];
+      proj_coeffs<M>(hp, rp, sb.c[0]);
+      __syncwarp();
+      project_apply<M>(bv.tab, sb.cell[1], sb.X1, sb.X2, sb.c[0], pass_mask(hp, rp), v);
+#pragma unroll
+      for (int t = 0; t < T; ++t) v[t] = v[t] - sb.cell[0][item_pos<M>(t)];
     }
+    store_cell_regs<M>(&bv.hdr->h, k, v, sb.cp[0]);
     __syncwarp();
-    store_cell<M>(&bv.hdr->h, k, sb.R, sb.cp);
   }
 }
 
@@ -237,22 +283,25 @@ __global__ void __launch_bounds__(WPB * 32) k_defect(DevField res, DevField rhs,
 template <int M>
 __global__ void k_norm_partial(DevField res, DevField field, double* partial) {
   __shared__ double sh[32];
-  __shared__ uint32_t alpha[Cfg<M>::N];
-  build_alpha<M>(alpha);
-  __syncthreads();
-  const Items<M> it(alpha);
   const int cells = res.nx * res.ny;
   const int chunk = (cells + gridDim.x - 1) / gridDim.x;
   const int lo = blockIdx.x * chunk, hi = min(cells, lo + chunk);
   const int warps = blockDim.x / 32, wid = threadIdx.x >> 5, lane = lane_id();
   double fact[Cfg<M>::T];
+  int deg[Cfg<M>::T];
+  bool valid[Cfg<M>::T];
 #pragma unroll
   for (int t = 0; t < Cfg<M>::T; ++t) {
+    const int k = lane + 32 * t;
+    valid[t] = k < Cfg<M>::N;
+    int a1 = 0, a2 = 0, a3 = 0;
+    if (valid[t]) decode(k, a1, a2, a3);
     double f = 1.0;
-    for (int q = 2; q <= it.a1(t); ++q) f *= q;
-    for (int q = 2; q <= it.a2(t); ++q) f *= q;
-    for (int q = 2; q <= it.a3(t); ++q) f *= q;
+    for (int q = 2; q <= a1; ++q) f *= q;
+    for (int q = 2; q <= a2; ++q) f *= q;
+    for (int q = 2; q <= a3; ++q) f *= q;
     fact[t] = f;
+    deg[t] = a1 + a2 + a3;
   }
   double v = 0.0;
   for (int k = lo + wid; k < hi; k += warps) {
@@ -261,12 +310,11 @@ __global__ void k_norm_partial(DevField res, DevField field, double* partial) {
     double cell = 0.0;
 #pragma unroll
     for (int t = 0; t < Cfg<M>::T; ++t) {
-      if (!it.v(t)) continue;
+      if (!valid[t]) continue;
       double tp = 1.0;
-      const int dg = it.deg(t);
 #pragma unroll
       for (int e = 1; e <= M; ++e)
-        if (e <= dg) tp *= theta;
+        if (e <= deg[t]) tp *= theta;
       const double r = res.c[(size_t)k * Cfg<M>::NP + lane + 32 * t];
       cell += fact[t] * tp * r * r;
     }
@@ -288,31 +336,127 @@ inline int grid_blocks(int cells) {
   return need < 148 * 16 ? need : 148 * 16;
 }
 
+template <typename K>
+inline void set_smem(K kernel, size_t bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// Thread-granular path (kernels_v3.cuh) for orders 3..6; warp-per-cell above
+// for orders 7, 8 (their per-thread vectors would not fit shared memory).
+template <int M>
+constexpr bool use_tc() { return M <= 6; }
+
+int tc_sweep_blocks(const void* kernel, size_t smem);
+tc::SegPlan tc_seg_plan(momg_field* f);
+
 // ---------------------------------------------------- templated launchers
 template <int M>
 struct Launch {
-  static size_t smem() { return BlockSmem<M>::bytes(WPB); }
+  static size_t smem(int order) {
+    return order == 2 ? BlockSmem<M, 2>::bytes(WPB) : BlockSmem<M, 1>::bytes(WPB);
+  }
   static void attrs() {
     static bool done = false;
     if (done) return;
-    const int s = (int)smem();
-    cudaFuncSetAttribute(k_residual<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-    cudaFuncSetAttribute(k_sweep_diag<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-    cudaFuncSetAttribute(k_restrict_sol<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-    cudaFuncSetAttribute(k_restrict_res<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-    cudaFuncSetAttribute(k_fas_correct<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-    cudaFuncSetAttribute(k_defect<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+    set_smem(k_residual<M, 1>, smem(1));
+    set_smem(k_residual<M, 2>, smem(2));
+    set_smem(k_sweep_diag<M, 1>, smem(1));
+    set_smem(k_sweep_diag<M, 2>, smem(2));
+    set_smem(k_restrict_sol<M>, smem(1));
+    set_smem(k_restrict_res<M>, smem(1));
+    set_smem(k_fas_correct<M>, smem(1));
+    set_smem(k_defect<M>, smem(1));
     done = true;
   }
+  static void tc_attrs() {
+    if constexpr (use_tc<M>()) {
+      static bool done = false;
+      if (done) return;
+      const size_t s = tc::TSmem<M>::bytes;
+      set_smem(tc::k3_residual<M, 1>, s);
+      set_smem(tc::k3_residual<M, 2>, s);
+      set_smem(tc::k3_sweep<M, 1>, s);
+      set_smem(tc::k3_sweep<M, 2>, s);
+      set_smem(tc::k3_sweep_diag<M, 1>, s);
+      set_smem(tc::k3_sweep_diag<M, 2>, s);
+      set_smem(tc::k3_restrict_sol<M>, s);
+      set_smem(tc::k3_restrict_res<M>, s);
+      set_smem(tc::k3_fas<M>, s);
+      set_smem(tc::k3_defect<M>, s);
+      done = true;
+    }
+  }
+  static int tc_grid(int work, int per_block) {
+    const int need = (work + per_block - 1) / per_block;
+    return need < 148 * 8 ? need : 148 * 8;
+  }
   static void residual(const DevCtx& ctx, const momg_field* f, momg_field* out) {
+    if constexpr (use_tc<M>()) {
+      tc_attrs();
+      const int g = tc_grid(f->nx * f->ny, tc::SEG);
+      if (ctx.order == 2)
+        tc::k3_residual<M, 2><<<g, tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(f->dev(), out->dev(), ctx, momg_rt::err_dev());
+      else
+        tc::k3_residual<M, 1><<<g, tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(f->dev(), out->dev(), ctx, momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     attrs();
-    k_residual<M><<<grid_blocks(f->nx * f->ny), WPB * 32, smem(), momg_rt::stream()>>>(
-        f->dev(), out->dev(), ctx, momg_rt::err_dev());
+    const int g = grid_blocks(f->nx * f->ny);
+    if (ctx.order == 2)
+      k_residual<M, 2><<<g, WPB * 32, smem(2), momg_rt::stream()>>>(f->dev(), out->dev(), ctx,
+                                                                   momg_rt::err_dev());
+    else
+      k_residual<M, 1><<<g, WPB * 32, smem(1), momg_rt::stream()>>>(f->dev(), out->dev(), ctx,
+                                                                   momg_rt::err_dev());
     momg_rt::count_launch(1);
   }
   static void sweep(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int* order) {
+    if constexpr (use_tc<M>()) {
+      tc_attrs();
+      const DevField fd = f->dev();
+      const DevField rd = rhs ? rhs->dev() : fd;
+      int has_rhs = rhs != nullptr;
+      DevErr* err = momg_rt::err_dev();
+      DevCtx c = ctx;
+      if (persistent_sweep_enabled()) {
+        tc::SegPlan plan = tc_seg_plan(f);
+        plan.nsweeps = 4;
+        for (int s = 0; s < 8; ++s) plan.dirs[s] = order[s & 3];
+        const void* kern = ctx.order == 2 ? (const void*)tc::k3_sweep<M, 2> : (const void*)tc::k3_sweep<M, 1>;
+        int nb = tc_sweep_blocks(kern, tc::TSmem<M>::bytes);
+        DevField fa = fd, ra = rd;
+        void* args[] = {&fa, &ra, &has_rhs, &c, &err, &plan};
+        cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(tc::VS), args, tc::TSmem<M>::bytes,
+                                    momg_rt::stream());
+        momg_rt::count_launch(1);
+        return;
+      }
+      static const int dirs4[4][2] = {{1, 1}, {0, 1}, {0, 0}, {1, 0}};
+      const int nx = f->nx, ny = f->ny;
+      for (int s = 0; s < 4; ++s) {
+        const int* dir = dirs4[order[s]];
+        for (int d = 0; d <= nx + ny - 2; ++d) {
+          const int lo = d - (ny - 1) > 0 ? d - (ny - 1) : 0;
+          const int hi = d < nx - 1 ? d : nx - 1;
+          const int count = hi - lo + 1;
+          const int g = (count + tc::SEG - 1) / tc::SEG;
+          if (ctx.order == 2)
+            tc::k3_sweep_diag<M, 2><<<g, tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(
+                fd, rd, has_rhs, ctx, err, dir[0], dir[1], d, lo, count);
+          else
+            tc::k3_sweep_diag<M, 1><<<g, tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(
+                fd, rd, has_rhs, ctx, err, dir[0], dir[1], d, lo, count);
+        }
+        momg_rt::count_launch(nx + ny - 1);
+      }
+      return;
+    }
     if (persistent_sweep_enabled()) {
-      PersistentSweep<M>::run(ctx, f, rhs, order);
+      if (ctx.order == 2)
+        PersistentSweep<M, 2>::run(ctx, f, rhs, order);
+      else
+        PersistentSweep<M, 1>::run(ctx, f, rhs, order);
       return;
     }
     attrs();
@@ -326,34 +470,68 @@ struct Launch {
         const int lo = d - (ny - 1) > 0 ? d - (ny - 1) : 0;
         const int hi = d < nx - 1 ? d : nx - 1;
         const int count = hi - lo + 1;
-        k_sweep_diag<M><<<(count + WPB - 1) / WPB, WPB * 32, smem(), momg_rt::stream()>>>(
-            fd, rd, rhs != nullptr, ctx, momg_rt::err_dev(), dir[0], dir[1], d, lo, count);
+        const int g = (count + WPB - 1) / WPB;
+        if (ctx.order == 2)
+          k_sweep_diag<M, 2><<<g, WPB * 32, smem(2), momg_rt::stream()>>>(
+              fd, rd, rhs != nullptr, ctx, momg_rt::err_dev(), dir[0], dir[1], d, lo, count);
+        else
+          k_sweep_diag<M, 1><<<g, WPB * 32, smem(1), momg_rt::stream()>>>(
+              fd, rd, rhs != nullptr, ctx, momg_rt::err_dev(), dir[0], dir[1], d, lo, count);
       }
       momg_rt::count_launch(nx + ny - 1);
     }
   }
   static void restrict_sol(const momg_field* fine, momg_field* coarse) {
+    if constexpr (use_tc<M>()) {
+      tc_attrs();
+      tc::k3_restrict_sol<M><<<tc_grid(coarse->nx * coarse->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes,
+                               momg_rt::stream()>>>(fine->dev(), coarse->dev(), momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     attrs();
-    k_restrict_sol<M><<<grid_blocks(coarse->nx * coarse->ny), WPB * 32, smem(),
+    k_restrict_sol<M><<<grid_blocks(coarse->nx * coarse->ny), WPB * 32, smem(1),
                         momg_rt::stream()>>>(fine->dev(), coarse->dev(), momg_rt::err_dev());
     momg_rt::count_launch(1);
   }
   static void restrict_res(const momg_field* arrays, const momg_field* coarse, momg_field* out) {
+    if constexpr (use_tc<M>()) {
+      tc_attrs();
+      tc::k3_restrict_res<M><<<tc_grid(coarse->nx * coarse->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes,
+                               momg_rt::stream()>>>(arrays->dev(), coarse->dev(), out->dev(),
+                                                    momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     attrs();
-    k_restrict_res<M><<<grid_blocks(coarse->nx * coarse->ny), WPB * 32, smem(),
+    k_restrict_res<M><<<grid_blocks(coarse->nx * coarse->ny), WPB * 32, smem(1),
                         momg_rt::stream()>>>(arrays->dev(), coarse->dev(), out->dev(),
                                              momg_rt::err_dev());
     momg_rt::count_launch(1);
   }
   static void fas(momg_field* fine, const momg_field* before, const momg_field* after) {
+    if constexpr (use_tc<M>()) {
+      tc_attrs();
+      tc::k3_fas<M><<<tc_grid(fine->nx * fine->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(
+          fine->dev(), before->dev(), after->dev(), momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     attrs();
-    k_fas_correct<M><<<grid_blocks(fine->nx * fine->ny), WPB * 32, smem(), momg_rt::stream()>>>(
+    k_fas_correct<M><<<grid_blocks(fine->nx * fine->ny), WPB * 32, smem(1), momg_rt::stream()>>>(
         fine->dev(), before->dev(), after->dev(), momg_rt::err_dev());
     momg_rt::count_launch(1);
   }
   static void defect(const momg_field* res, const momg_field* rhs, momg_field* out) {
+    if constexpr (use_tc<M>()) {
+      tc_attrs();
+      tc::k3_defect<M><<<tc_grid(res->nx * res->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(
+          res->dev(), rhs ? rhs->dev() : res->dev(), rhs != nullptr, out->dev(), momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     attrs();
-    k_defect<M><<<grid_blocks(res->nx * res->ny), WPB * 32, smem(), momg_rt::stream()>>>(
+    k_defect<M><<<grid_blocks(res->nx * res->ny), WPB * 32, smem(1), momg_rt::stream()>>>(
         res->dev(), rhs ? rhs->dev() : res->dev(), rhs != nullptr, out->dev(),
         momg_rt::err_dev());
     momg_rt::count_launch(1);

@@ -1,29 +1,30 @@
-// Per-cell warp routines: face fluxes, collision, cell residual, the local
-// update with grad_normalize and the dt/2 retry, and the transfer-operator
-// bodies.  Each routine is executed by one full warp on one cell; vectors
-// live in the warp's shared-memory buffers (WarpBuf), problem constants and
-// field descriptors in the block header (BlockHdr), both in shared memory.
+// Per-cell warp routines: stencil prefetch, face fluxes, collision, the cell
+// residual, the local update with grad_normalize and the dt/2 retry.  One
+// full warp works on one cell; vectors live in the warp's shared-memory
+// buffers (WarpBuf), descriptors in the block header (BlockHdr).
 #pragma once
 
 #include "momg_device.cuh"
 
 namespace momg_gpu {
 
-template <int M>
+// Stencil slots: 0 self, 1 x-, 2 x+, 3 y-, 4 y+, 5 x--, 6 x++, 7 y--, 8 y++.
+template <int ORDER>
+struct Stencil {
+  static constexpr int NCELL = ORDER == 2 ? 9 : 5;
+};
+
+template <int M, int ORDER>
 struct WarpBuf {
-  static constexpr int NP = Cfg<M>::NP, KT = Cfg<M>::KT;
-  double S[NP];   // the cell's own state
-  double A[NP];   // face state / projection scratch
-  double A2[NP];
-  double B[NP];
-  double B2[NP];
-  double F1[NP];  // face fluxes in the cell basis
-  double F2[NP];
-  double R[NP];   // residual accumulator
-  double Kup[KT];
-  double Klo[KT];
-  double cp[4];   // the cell's basis params
-  double par[8];  // face-state / scratch params shared by the lanes
+  using C = Cfg<M>;
+  static constexpr int NB = C::NB;
+  double cell[Stencil<ORDER>::NCELL][NB];  // prefetched stencil (slot N = 0)
+  double LA[NB], UB[NB];                   // reconstructed face states / flux scratch
+  double X1[NB], X2[NB], Y1[NB], Y2[NB];   // projection ping-pong scratch
+  double Kup[C::KT], Klo[C::KT];           // folded half-flux kernels
+  double c[4][C::PC];                      // projection coefficients
+  double cp[Stencil<ORDER>::NCELL][4];     // stencil params
+  double par[8];                           // face-state params (lower, upper)
 };
 
 struct BlockHdr {
@@ -31,41 +32,37 @@ struct BlockHdr {
   DevField f, g, h, o;
 };
 
-template <int M>
+template <int M, int ORDER>
 struct BlockSmem {
-  static constexpr size_t alpha_bytes = ((Cfg<M>::N * 4 + 31) / 32) * 32;
-  static constexpr size_t hdr_bytes = ((sizeof(BlockHdr) + 31) / 32) * 32;
+  static constexpr size_t tab_bytes = ((Cfg<M>::WORDS * 32 * 4 + 127) / 128) * 128;
+  static constexpr size_t hdr_bytes = ((sizeof(BlockHdr) + 127) / 128) * 128;
   static constexpr size_t bytes(int warps) {
-    return hdr_bytes + alpha_bytes + sizeof(WarpBuf<M>) * (size_t)warps;
+    return hdr_bytes + tab_bytes + sizeof(WarpBuf<M, ORDER>) * (size_t)warps;
   }
 };
 
 struct BlockView {
   BlockHdr* hdr;
-  uint32_t* alpha;
+  uint32_t* tab;
   unsigned char* warps;
 };
 
-template <int M>
-__device__ __forceinline__ BlockView block_view(unsigned char* raw) {
-  BlockView v;
-  v.hdr = reinterpret_cast<BlockHdr*>(raw);
-  v.alpha = reinterpret_cast<uint32_t*>(raw + BlockSmem<M>::hdr_bytes);
-  v.warps = raw + BlockSmem<M>::hdr_bytes + BlockSmem<M>::alpha_bytes;
-  return v;
-}
-template <int M>
-__device__ __forceinline__ WarpBuf<M>& warp_buf(const BlockView& v) {
-  return reinterpret_cast<WarpBuf<M>*>(v.warps)[threadIdx.x >> 5];
+template <int M, int ORDER>
+__device__ __forceinline__ WarpBuf<M, ORDER>& warp_buf(const BlockView& v) {
+  return reinterpret_cast<WarpBuf<M, ORDER>*>(v.warps)[threadIdx.x >> 5];
 }
 
-// Block prologue: copy the launch descriptors to shared memory and build the
-// multi-index table.
-template <int M>
+// Block prologue: launch descriptors to shared memory, index tables, zero
+// slots of every warp buffer.
+template <int M, int ORDER>
 __device__ __forceinline__ BlockView block_setup(unsigned char* raw, const DevCtx* ctx,
                                                  const DevField* f, const DevField* g,
                                                  const DevField* h, const DevField* o) {
-  BlockView v = block_view<M>(raw);
+  using S = BlockSmem<M, ORDER>;
+  BlockView v;
+  v.hdr = reinterpret_cast<BlockHdr*>(raw);
+  v.tab = reinterpret_cast<uint32_t*>(raw + S::hdr_bytes);
+  v.warps = raw + S::hdr_bytes + S::tab_bytes;
   if (threadIdx.x == 0) {
     if (ctx) v.hdr->ctx = *ctx;
     if (f) v.hdr->f = *f;
@@ -73,7 +70,11 @@ __device__ __forceinline__ BlockView block_setup(unsigned char* raw, const DevCt
     if (h) v.hdr->h = *h;
     if (o) v.hdr->o = *o;
   }
-  build_alpha<M>(v.alpha);
+  build_tables<M>(v.tab);
+  // zero the whole warp area once: zero slots stay zero forever
+  double* z = reinterpret_cast<double*>(v.warps);
+  const int nz = (int)(sizeof(WarpBuf<M, ORDER>) / 8) * (blockDim.x / 32);
+  for (int q = threadIdx.x; q < nz; q += blockDim.x) z[q] = 0.0;
   __syncthreads();
   return v;
 }
@@ -104,31 +105,42 @@ __device__ __forceinline__ int code_of(int what) {
   }
 }
 
-// L2-coherent global loads/stores: values written by other SMs during a
-// persistent sweep are observed after the flag acquire.
+// L2-coherent global access (values written by other SMs during a persistent
+// sweep are observed after the flag acquire).
 __device__ __forceinline__ double ldg_cg(const double* p) { return __ldcg(p); }
 
-// Loads a cell's coefficients into smem `dst` and its params into `prm`
-// (smem, 4 doubles); synced on return.
+// Issues the loads of one cell record into smem (no sync).
 template <int M>
-__device__ __forceinline__ void load_cell(const DevField* f, size_t cell, double* dst, double* prm) {
-  constexpr int NP = Cfg<M>::NP;
-  const double* src = f->c + cell * NP;
+__device__ __forceinline__ void load_cell_async(const DevField* f, size_t cell, double* dst,
+                                                double* prm) {
+  const double* src = f->c + cell * Cfg<M>::NP;
   const int lane = lane_id();
-  for (int k = lane; k < Cfg<M>::N; k += 32) dst[k] = ldg_cg(src + k);
+#pragma unroll
+  for (int t = 0; t < Cfg<M>::T; ++t) {
+    const int k = lane + 32 * t;
+    if (t < Cfg<M>::T - 1 || k < Cfg<M>::N) dst[k] = ldg_cg(src + k);
+  }
   if (lane < 4) prm[lane] = ldg_cg(f->p + cell * 4 + lane);
-  __syncwarp();
 }
 
 template <int M>
-__device__ __forceinline__ void store_cell(const DevField* f, size_t cell, const double* src,
-                                           const double* prm) {
-  constexpr int NP = Cfg<M>::NP;
-  const int lane = lane_id();
-  double* dst = f->c + cell * NP;
-  for (int k = lane; k < Cfg<M>::N; k += 32) __stcg(dst + k, src[k]);
-  if (lane < 4) __stcg(f->p + cell * 4 + lane, prm[lane]);
+__device__ __forceinline__ void load_cell(const DevField* f, size_t cell, double* dst, double* prm) {
+  load_cell_async<M>(f, cell, dst, prm);
   __syncwarp();
+}
+
+// Writes registers v (+ params prm) to global memory.
+template <int M>
+__device__ __forceinline__ void store_cell_regs(const DevField* f, size_t cell, const double* v,
+                                                const double* prm) {
+  const int lane = lane_id();
+  double* dst = f->c + cell * Cfg<M>::NP;
+#pragma unroll
+  for (int t = 0; t < Cfg<M>::T; ++t) {
+    const int k = lane + 32 * t;
+    if (t < Cfg<M>::T - 1 || k < Cfg<M>::N) __stcg(dst + k, v[t]);
+  }
+  if (lane < 4) __stcg(f->p + cell * 4 + lane, prm[lane]);
 }
 
 __device__ __forceinline__ P4 p4(const double* p) {
@@ -140,77 +152,110 @@ __device__ __forceinline__ P4 p4(const double* p) {
   return r;
 }
 
-// Face state of cell (i, j) on its (axis, high) face (spatial.cpp:34-80) into
-// dst / prm: order 1 -> the cell; order 2 -> central slope from the
-// neighbours along the axis (zero at wall-adjacent cells), with the
-// nonpositive-temperature fallback to the cell value (safe_face_state,
-// spatial.cpp:53-60).
-template <int M>
-__device__ __noinline__ void face_state(const DevField* f, int order, int i, int j, int axis,
-                                        bool high, double* dst, double* prm) {
-  constexpr int NP = Cfg<M>::NP;
-  const size_t cell = (size_t)j * f->nx + i;
-  load_cell<M>(f, cell, dst, prm);
-  if (order == 1) return;
-  const int m = axis == 0 ? i : j;
-  const int last = (axis == 0 ? f->nx : f->ny) - 1;
-  if (m == 0 || m == last) return;  // zero slope: w = cell (+ off * 0)
-  const size_t lo = axis == 0 ? cell - 1 : cell - f->nx;
-  const size_t hi = axis == 0 ? cell + 1 : cell + f->nx;
-  const double h = axis == 0 ? f->xc[i + 1] - f->xc[i - 1] : f->yc[j + 1] - f->yc[j - 1];
-  const double off = (high ? 0.5 : -0.5) * (axis == 0 ? f->dx[i] : f->dy[j]);
-  const double wsp = prm[3] + off * ((ldg_cg(f->p + hi * 4 + 3) - ldg_cg(f->p + lo * 4 + 3)) / h);
-  if (!(wsp > 0.0)) return;  // NonphysicalReconstruction -> first order
-  const int lane = lane_id();
-  const double rh = 1.0 / h;
-  for (int k = lane; k < Cfg<M>::N; k += 32) {
-    const double s = (ldg_cg(f->c + hi * NP + k) - ldg_cg(f->c + lo * NP + k)) * rh;
-    dst[k] = fma(off, s, dst[k]);
+// Prefetches the stencil of cell (i, j) (radius 1 or 2 cross) into sb.cell
+// with one batch of independent loads; synced on return.
+template <int M, int ORDER>
+__device__ __forceinline__ void load_stencil(const DevField* f, int i, int j,
+                                             WarpBuf<M, ORDER>& sb) {
+  const size_t c = (size_t)j * f->nx + i;
+  load_cell_async<M>(f, c, sb.cell[0], sb.cp[0]);
+  if (i > 0) load_cell_async<M>(f, c - 1, sb.cell[1], sb.cp[1]);
+  if (i < f->nx - 1) load_cell_async<M>(f, c + 1, sb.cell[2], sb.cp[2]);
+  if (j > 0) load_cell_async<M>(f, c - f->nx, sb.cell[3], sb.cp[3]);
+  if (j < f->ny - 1) load_cell_async<M>(f, c + f->nx, sb.cell[4], sb.cp[4]);
+  if (ORDER == 2) {
+    if (i > 1) load_cell_async<M>(f, c - 2, sb.cell[5 % Stencil<ORDER>::NCELL], sb.cp[5 % Stencil<ORDER>::NCELL]);
+    if (i < f->nx - 2) load_cell_async<M>(f, c + 2, sb.cell[6 % Stencil<ORDER>::NCELL], sb.cp[6 % Stencil<ORDER>::NCELL]);
+    if (j > 1) load_cell_async<M>(f, c - 2 * (size_t)f->nx, sb.cell[7 % Stencil<ORDER>::NCELL], sb.cp[7 % Stencil<ORDER>::NCELL]);
+    if (j < f->ny - 2) load_cell_async<M>(f, c + 2 * (size_t)f->nx, sb.cell[8 % Stencil<ORDER>::NCELL], sb.cp[8 % Stencil<ORDER>::NCELL]);
   }
-  __syncwarp();
-  if (lane < 3) prm[lane] = prm[lane] + off * ((ldg_cg(f->p + hi * 4 + lane) - ldg_cg(f->p + lo * 4 + lane)) / h);
-  if (lane == 3) prm[3] = wsp;
   __syncwarp();
 }
 
+// face_state + safe_face_state (spatial.cpp:34-80) of the stencil cell in
+// slot `s` on its (axis, high) face, for second order: central slope from
+// slots `lo`/`hi`, zero slope at wall-adjacent cells (position m == 0 or
+// last), nonpositive-temperature fallback to the cell.  Returns the buffer
+// holding the state (the cell buffer itself when unchanged) and writes the
+// params to prm.
+template <int M, int ORDER>
+__device__ __forceinline__ const double* face_state(const DevField* f, WarpBuf<M, ORDER>& sb, int s,
+                                                    int lo, int hi, int m, int last, double h,
+                                                    double off, double* dst, double* prm) {
+  const int lane = lane_id();
+  if (ORDER == 1 || m == 0 || m == last) {
+    if (lane < 4) prm[lane] = sb.cp[s][lane];
+    return sb.cell[s];
+  }
+  const double* cs = sb.cell[s];
+  const double* cl = sb.cell[lo];
+  const double* ch = sb.cell[hi];
+  const double wsp = sb.cp[s][3] + off * ((sb.cp[hi][3] - sb.cp[lo][3]) / h);
+  if (!(wsp > 0.0)) {  // NonphysicalReconstruction -> first-order value
+    if (lane < 4) prm[lane] = sb.cp[s][lane];
+    return sb.cell[s];
+  }
+  const double rh = 1.0 / h;
+#pragma unroll
+  for (int t = 0; t < Cfg<M>::T; ++t) {
+    const int k = lane + 32 * t;
+    if (t < Cfg<M>::T - 1 || k < Cfg<M>::N) dst[k] = fma(off, (ch[k] - cl[k]) * rh, cs[k]);
+  }
+  if (lane < 3) prm[lane] = sb.cp[s][lane] + off * ((sb.cp[hi][lane] - sb.cp[lo][lane]) / h);
+  if (lane == 3) prm[3] = wsp;
+  return dst;
+}
+
 // ------------------------------------------------------------ grad_normalize
-// projection.hpp:96-121 on the vector in smem X with basis prm (smem, updated
-// in place); Y is scratch.  Returns W_NONE or the failure kind.
-template <int M>
-__device__ __noinline__ int grad_normalize_smem(const uint32_t* alpha, double* X, double* Y,
-                                                double* prm, double* bad) {
+// projection.hpp:96-121 on the vector held in smem `X` and registers v with
+// basis prm (smem, updated); Y, Z scratch.  Returns W_NONE or the failure
+// kind; on success *out points at the buffer holding the result (== v).
+template <int M, int ORDER>
+__device__ __forceinline__ int grad_normalize(const uint32_t* tab, WarpBuf<M, ORDER>& sb, double* X,
+                                              double* Y, double* Z, double* prm, double* v,
+                                              double* bad, const double** out) {
   const double rel_tol = 1e-12;
+  const double* cur = X;
   for (int iter = 0; iter < 30; ++iter) {
-    const double rho = X[0];
+    const double rho = cur[0];
     if (!isfinite(rho) || !(rho > 0.0)) {
       *bad = rho;
       return W_GRAD_RHO;
     }
-    if (grad_defect(X) <= rel_tol) return W_NONE;
+    if (grad_defect(cur) <= rel_tol) {
+      *out = cur;
+      return W_NONE;
+    }
     P4 to;
-    to.v[0] = rep_u(X, prm, 0);
-    to.v[1] = rep_u(X, prm, 1);
-    to.v[2] = rep_u(X, prm, 2);
-    to.v[3] = rep_theta(X, prm);
+    const P4 from = p4(prm);
+    to.v[0] = rep_u(cur, prm, 0);
+    to.v[1] = rep_u(cur, prm, 1);
+    to.v[2] = rep_u(cur, prm, 2);
+    to.v[3] = rep_theta(cur, prm);
     if (!isfinite(to.v[3]) || !(to.v[3] > 0.0)) {
       *bad = to.v[3];
       return W_GRAD_THETA;
     }
     if (!isfinite(to.v[0]) || !isfinite(to.v[1]) || !isfinite(to.v[2])) return W_GRAD_U;
-    project_smem<M>(alpha, X, Y, p4(prm), to, X);
-    if (lane_id() < 4) prm[lane_id()] = to.v[lane_id()];
+    proj_coeffs<M>(from, to, sb.c[3]);
     __syncwarp();
+    if (lane_id() < 4) prm[lane_id()] = to.v[lane_id()];
+    double* s1 = cur == X ? Y : (cur == Y ? Z : X);
+    double* s2 = cur == X ? Z : (cur == Y ? X : Y);
+    cur = project_apply<M>(tab, cur, s1, s2, sb.c[3], pass_mask(from, to), v);
   }
-  if (grad_defect(X) > rel_tol) return W_GRAD_CAP;
+  if (grad_defect(cur) > rel_tol) return W_GRAD_CAP;
+  *out = cur;
   return W_NONE;
 }
 
 // ----------------------------------------------------------------- collision
-// collision_coeffs (collision.hpp:120-127): dst = nu (f_eq - f) in the cell's
-// own basis, BGK or Shakhov (extract_macro moment_rep.hpp:116-146).
+// collision_coeffs (collision.hpp:120-127): Q = nu (f_eq - f) in the cell's
+// own basis, BGK or Shakhov (extract_macro moment_rep.hpp:116-146), into
+// registers.
 template <int M>
-__device__ __noinline__ int collision_smem(const uint32_t* alpha, const double* S,
-                                           const double* cp, const DevCtx* ctx, double* dst) {
+__device__ __forceinline__ int collision(const uint32_t* tab, const double* S, const double* cp,
+                                         const DevCtx* ctx, double* Q) {
   const double rho = S[0];
   if (!(rho > 0.0)) return W_MACRO_RHO;
   const double theta = cp[3];
@@ -225,35 +270,38 @@ __device__ __noinline__ int collision_smem(const uint32_t* alpha, const double* 
     q[1] = 2.0 * S[flat3(0, 3, 0)] + S[flat3(2, 1, 0)] + S[flat3(0, 3, 0)] + S[flat3(0, 1, 2)];
     q[2] = 2.0 * S[flat3(0, 0, 3)] + S[flat3(2, 0, 1)] + S[flat3(0, 2, 1)] + S[flat3(0, 0, 3)];
   }
-  const Items<M> it(alpha);
   const int lane = lane_id();
 #pragma unroll
   for (int t = 0; t < Cfg<M>::T; ++t) {
-    if (!it.v(t)) continue;
     const int k = lane + 32 * t;
     double eq = k == 0 ? rho : 0.0;
-    const int a1 = it.a1(t), a2 = it.a2(t), a3 = it.a3(t);
-    if (shakhov && a1 + a2 + a3 == 3 && !(a1 == 1 && a2 == 1 && a3 == 1)) {
-      const int d = (a1 & 1) ? 0 : ((a2 & 1) ? 1 : 2);
-      eq = ctx->shakhov_w * q[d];
+    if (shakhov) {
+      const uint32_t ms = misc<M>(tab, t);
+      const int a1 = byte_of(ms, 0), a2 = byte_of(ms, 1), a3 = byte_of(ms, 2);
+      if (a1 + a2 + a3 == 3 && !(a1 == 1 && a2 == 1 && a3 == 1) && k < Cfg<M>::N) {
+        const int d = (a1 & 1) ? 0 : ((a2 & 1) ? 1 : 2);
+        eq = ctx->shakhov_w * q[d];
+      }
     }
-    dst[k] = nu * (eq - S[k]);
+    Q[t] = nu * (eq - S[item_pos<M>(t)]);
   }
-  __syncwarp();
   return W_NONE;
 }
 
 // ----------------------------------------------------------------- face flux
 // Flux through face (axis, high) of cell (i, j), projected into the cell
-// basis cp (the `face` lambda of cell_residual, spatial.cpp:106-124), into
-// dst.  The cell's own state is in sb.S.  Returns W_NONE or a failure kind.
-template <int M>
-__device__ __noinline__ int cell_face(const DevField* f, const DevCtx* ctx, const uint32_t* alpha,
-                                      int i, int j, int axis, bool high, const double* cp,
-                                      WarpBuf<M>& sb, double* dst) {
+// basis (the `face` lambda of cell_residual, spatial.cpp:106-124), into
+// registers F.  Stencil in sb.cell / sb.cp.  Returns W_NONE or a failure.
+template <int M, int ORDER>
+__device__ __forceinline__ int cell_face(const DevField* f, const DevCtx* ctx, const uint32_t* tab,
+                                         int i, int j, int axis, bool high, WarpBuf<M, ORDER>& sb,
+                                         double* F) {
+  constexpr int T = Cfg<M>::T;
   const int lane = lane_id();
   const bool at_wall = axis == 0 ? (high ? i == f->nx - 1 : i == 0)
                                  : (high ? j == f->ny - 1 : j == 0);
+  const P4 cp = p4(sb.cp[0]);
+  double out[T];
   P4 fp;
   if (at_wall) {
     // wall_flux, flux.cpp:105-130
@@ -264,81 +312,117 @@ __device__ __noinline__ int cell_face(const DevField* f, const DevCtx* ctx, cons
     if (!(fp.v[3] > 0.0)) return W_PROJ_SPREAD;
     const double rs = sqrt(fp.v[3]);
     half_kernels<M>(0.0, rs, sb.Kup, sb.Klo);
-    vcopy<M>(sb.A, sb.S);
-    project_smem<M>(alpha, sb.A, sb.A2, p4(cp), fp, sb.A);
+    proj_coeffs<M>(cp, fp, sb.c[0]);
+    proj_coeffs<M>(fp, cp, sb.c[2]);
+    __syncwarp();
+    double v[T];
+    const double* in_w = project_apply<M>(tab, sb.cell[0], sb.X1, sb.X2, sb.c[0], pass_mask(cp, fp), v);
     const double* Kout = high ? sb.Kup : sb.Klo;
     const double* Kin = high ? sb.Klo : sb.Kup;
-    half_sum<M>(alpha, sb.A, Kout, nullptr, nullptr, axis, rs, sb.B);
-    const double o0 = sb.B[0];
+    half_sum<M>(tab, in_w, Kout, nullptr, nullptr, axis, out);
+    const double o0 = __shfl_sync(FULL, out[0], 0);
     const double in0 = Kin[0];
     if (in0 == 0.0) return W_WALL_DEGEN;
     const double wall_rho = -o0 / in0;
     if (!(wall_rho > 0.0)) return W_WALL_RHO;
-    // incoming unit-wall half flux: nonzero only at beta = p e_n
-    if (lane <= M) {
-      const int p = lane;
-      double v = Kin[p];
-      for (int e = 1; e <= p; ++e) v = v * rs * rcp_int(e);
-      const int k = flat3(axis == 0 ? p : 0, axis == 1 ? p : 0, axis == 2 ? p : 0);
-      sb.B[k] = fma(wall_rho, v, sb.B[k]);
+    // incoming unit-wall half flux: rs^p/p! K(0,p) at beta = p e_axis
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const uint32_t ms = misc<M>(tab, t);
+      const int p = byte_of(ms, axis);
+      const int tan = byte_of(ms, 0) + byte_of(ms, 1) + byte_of(ms, 2) - p;
+      if (tan == 0 && (t < T - 1 || lane + 32 * t < Cfg<M>::N)) out[t] = fma(wall_rho, Kin[p], out[t]);
     }
+    if (lane == 0) out[0] = 0.0;
+    store_items<M>(sb.LA, out);
     __syncwarp();
-    if (lane == 0) sb.B[0] = 0.0;
-    __syncwarp();
-    if (!project_smem<M>(alpha, sb.B, sb.B2, fp, p4(cp), dst)) return W_PROJ_SPREAD;
+    project_apply<M>(tab, sb.LA, sb.X1, sb.X2, sb.c[2], pass_mask(fp, cp), F);
     return W_NONE;
   }
-  // interior face, flux.cpp:77-97 with the geometric lo/hi roles of
-  // spatial.cpp:114-121
-  const int ni = axis == 0 ? (high ? i + 1 : i - 1) : i;
-  const int nj = axis == 1 ? (high ? j + 1 : j - 1) : j;
+  // interior face, flux.cpp:77-97, lo/hi roles of spatial.cpp:114-121
+  const int s_nb = axis == 0 ? (high ? 2 : 1) : (high ? 4 : 3);     // neighbour slot
+  const int s_nb2 = axis == 0 ? (high ? 6 : 5) : (high ? 8 : 7);    // neighbour's far slot
+  const int s_opp = axis == 0 ? (high ? 1 : 2) : (high ? 3 : 4);    // own opposite slot
+  const int pos = axis == 0 ? i : j;
+  const int last = (axis == 0 ? f->nx : f->ny) - 1;
+  const double* xc = axis == 0 ? f->xc : f->yc;
+  const double* dd = axis == 0 ? f->dx : f->dy;
   double* lp = sb.par;
   double* rp = sb.par + 4;
-  face_state<M>(f, ctx->order, high ? i : ni, high ? j : nj, axis, true, sb.A, lp);
-  face_state<M>(f, ctx->order, high ? ni : i, high ? nj : j, axis, false, sb.B, rp);
-  const double ul = rep_u(sb.A, lp, axis), ur = rep_u(sb.B, rp, axis);
-  const double cl = ctx->c_bound * sqrt(rep_theta(sb.A, lp));
-  const double cr = ctx->c_bound * sqrt(rep_theta(sb.B, rp));
+  const double* L;
+  const double* U;
+  if (high) {
+    // lower = self (slope from opp -> nb), upper = nb (slope from self -> nb2)
+    L = face_state<M, ORDER>(f, sb, 0, s_opp, s_nb, pos, last,
+                             ORDER == 2 && pos > 0 && pos < last ? xc[pos + 1] - xc[pos - 1] : 1.0,
+                             0.5 * dd[pos], sb.LA, lp);
+    U = face_state<M, ORDER>(f, sb, s_nb, 0, s_nb2 % Stencil<ORDER>::NCELL, pos + 1, last,
+                             ORDER == 2 && pos + 1 < last ? xc[pos + 2] - xc[pos] : 1.0,
+                             -0.5 * dd[pos + 1], sb.UB, rp);
+  } else {
+    L = face_state<M, ORDER>(f, sb, s_nb, s_nb2 % Stencil<ORDER>::NCELL, 0, pos - 1, last,
+                             ORDER == 2 && pos - 1 > 0 ? xc[pos] - xc[pos - 2] : 1.0,
+                             0.5 * dd[pos - 1], sb.LA, lp);
+    U = face_state<M, ORDER>(f, sb, 0, s_nb, s_opp, pos, last,
+                             ORDER == 2 && pos > 0 && pos < last ? xc[pos + 1] - xc[pos - 1] : 1.0,
+                             -0.5 * dd[pos], sb.UB, rp);
+  }
+  __syncwarp();
+  const double ul = rep_u(L, lp, axis), ur = rep_u(U, rp, axis);
+  const double cl = ctx->c_bound * sqrt(rep_theta(L, lp));
+  const double cr = ctx->c_bound * sqrt(rep_theta(U, rp));
   const double lminus = smin(ul - cl, ur - cr);
   const double lplus = smax(ul + cl, ur + cr);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) fp.v[q] = 0.5 * (lp[q] + rp[q]);
   const P4 lpv = p4(lp), rpv = p4(rp);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) fp.v[q] = 0.5 * (lpv.v[q] + rpv.v[q]);
+  if (!(fp.v[3] > 0.0)) return W_PROJ_SPREAD;
   if (lminus >= 0.0 || lplus <= 0.0) {
-    double* X = lminus >= 0.0 ? sb.A : sb.B;
-    double* Y = lminus >= 0.0 ? sb.A2 : sb.B2;
-    if (!project_smem<M>(alpha, X, Y, lminus >= 0.0 ? lpv : rpv, fp, X)) return W_PROJ_SPREAD;
-    full_flux<M>(alpha, X, fp.v[axis], fp.v[3], axis, Y);
-    return project_smem<M>(alpha, Y, X, fp, p4(cp), dst) ? W_NONE : W_PROJ_SPREAD;
+    const bool left = lminus >= 0.0;
+    proj_coeffs<M>(left ? lpv : rpv, fp, sb.c[0]);
+    proj_coeffs<M>(fp, cp, sb.c[2]);
+    __syncwarp();
+    double v[T];
+    const double* st = project_apply<M>(tab, left ? L : U, sb.X1, sb.X2, sb.c[0],
+                                        pass_mask(left ? lpv : rpv, fp), v);
+    full_flux<M>(tab, st, fp.v[axis], fp.v[3], axis, out);
+  } else {
+    const double rs = sqrt(fp.v[3]);
+    half_kernels<M>(fp.v[axis], rs, sb.Kup, sb.Klo);
+    proj_coeffs<M>(lpv, fp, sb.c[0]);
+    proj_coeffs<M>(rpv, fp, sb.c[1]);
+    proj_coeffs<M>(fp, cp, sb.c[2]);
+    __syncwarp();
+    double va[T], vb[T];
+    const double *pa, *pb;
+    project_apply2<M>(tab, L, sb.X1, sb.X2, sb.c[0], pass_mask(lpv, fp), va, U, sb.Y1, sb.Y2,
+                      sb.c[1], pass_mask(rpv, fp), vb, &pa, &pb);
+    half_sum<M>(tab, pa, sb.Kup, pb, sb.Klo, axis, out);
   }
-  if (!(fp.v[3] > 0.0)) return W_HALF_SPREAD;
-  const double rs = sqrt(fp.v[3]);
-  half_kernels<M>(fp.v[axis], rs, sb.Kup, sb.Klo);
-  if (!project_smem<M>(alpha, sb.A, sb.A2, lpv, fp, sb.A)) return W_PROJ_SPREAD;
-  project_smem<M>(alpha, sb.B, sb.B2, rpv, fp, sb.B);
-  half_sum<M>(alpha, sb.A, sb.Kup, sb.B, sb.Klo, axis, rs, sb.A2);
-  if (!project_smem<M>(alpha, sb.A2, sb.B2, fp, p4(cp), dst)) return W_PROJ_SPREAD;
+  __syncwarp();
+  store_items<M>(sb.LA, out);
+  __syncwarp();
+  project_apply<M>(tab, sb.LA, sb.X1, sb.X2, sb.c[2], pass_mask(fp, cp), F);
   return W_NONE;
 }
 
-// cell_residual (spatial.cpp:98-133): R = Q - (F_x+ - F_x-)/dx - (F_y+ - F_y-)/dy
-// in the cell basis, into sb.R.  The cell state must be in sb.S with params cp.
-template <int M>
-__device__ __noinline__ int cell_residual_smem(const DevField* f, const DevCtx* ctx,
-                                               const uint32_t* alpha, int i, int j,
-                                               const double* cp, WarpBuf<M>& sb) {
-  int w = collision_smem<M>(alpha, sb.S, cp, ctx, sb.R);
+// cell_residual (spatial.cpp:98-133) into registers R, stencil prefetched.
+template <int M, int ORDER>
+__device__ __forceinline__ int cell_residual(const DevField* f, const DevCtx* ctx, const uint32_t* tab,
+                                             int i, int j, WarpBuf<M, ORDER>& sb, double* R) {
+  constexpr int T = Cfg<M>::T;
+  int w = collision<M>(tab, sb.cell[0], sb.cp[0], ctx, R);
   if (w) return w;
-  if ((w = cell_face<M>(f, ctx, alpha, i, j, 0, true, cp, sb, sb.F1))) return w;
-  if ((w = cell_face<M>(f, ctx, alpha, i, j, 0, false, cp, sb, sb.F2))) return w;
-  const int lane = lane_id();
+  double Fp[T], Fm[T];
+  if ((w = cell_face<M, ORDER>(f, ctx, tab, i, j, 0, true, sb, Fp))) return w;
+  if ((w = cell_face<M, ORDER>(f, ctx, tab, i, j, 0, false, sb, Fm))) return w;
   const double dx = f->dx[i], dy = f->dy[j];
-  for (int k = lane; k < Cfg<M>::N; k += 32) sb.R[k] -= (sb.F1[k] - sb.F2[k]) / dx;
-  __syncwarp();
-  if ((w = cell_face<M>(f, ctx, alpha, i, j, 1, true, cp, sb, sb.F1))) return w;
-  if ((w = cell_face<M>(f, ctx, alpha, i, j, 1, false, cp, sb, sb.F2))) return w;
-  for (int k = lane; k < Cfg<M>::N; k += 32) sb.R[k] -= (sb.F1[k] - sb.F2[k]) / dy;
-  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < T; ++t) R[t] -= (Fp[t] - Fm[t]) / dx;
+  if ((w = cell_face<M, ORDER>(f, ctx, tab, i, j, 1, true, sb, Fp))) return w;
+  if ((w = cell_face<M, ORDER>(f, ctx, tab, i, j, 1, false, sb, Fm))) return w;
+#pragma unroll
+  for (int t = 0; t < T; ++t) R[t] -= (Fp[t] - Fm[t]) / dy;
   return W_NONE;
 }
 
@@ -353,35 +437,46 @@ __device__ __forceinline__ int local_dt(const DevCtx* ctx, const double* cp, dou
 }
 
 // sweep_cell (single_level.cpp:103-111) + update_delta / apply_update
-// (:44-70).  rhs may be null (empty RhsField).  Writes the updated cell, or
-// leaves it unchanged and returns the failure kind.
-template <int M>
-__device__ __noinline__ int sweep_cell_smem(const DevField* f, const DevField* rhs,
-                                            const DevCtx* ctx, const uint32_t* alpha, int i, int j,
-                                            WarpBuf<M>& sb, double* bad) {
+// (:44-70) for cell (i, j) whose stencil is prefetched.  rhs may be null.
+// Writes the updated cell, or leaves it and returns the failure kind.
+template <int M, int ORDER>
+__device__ __forceinline__ int sweep_cell(const DevField* f, const DevField* rhs, const DevCtx* ctx,
+                                          const uint32_t* tab, int i, int j, WarpBuf<M, ORDER>& sb,
+                                          double* bad) {
+  constexpr int T = Cfg<M>::T;
   const size_t cell = (size_t)j * f->nx + i;
-  load_cell<M>(f, cell, sb.S, sb.cp);
   double dt;
-  int w = local_dt(ctx, sb.cp, f->dx[i], f->dy[j], &dt);
+  int w = local_dt(ctx, sb.cp[0], f->dx[i], f->dy[j], &dt);
   if (w) return w;
-  w = cell_residual_smem<M>(f, ctx, alpha, i, j, sb.cp, sb);
+  double R[T];
+  w = cell_residual<M, ORDER>(f, ctx, tab, i, j, sb, R);
   if (w) return w;
   const int lane = lane_id();
   if (rhs) {
-    load_cell<M>(rhs, cell, sb.A, sb.par);
-    if (!project_smem<M>(alpha, sb.A, sb.A2, p4(sb.par), p4(sb.cp), sb.F1)) return W_PROJ_SPREAD;
-    for (int k = lane; k < Cfg<M>::N; k += 32) sb.R[k] -= sb.F1[k];
+    load_cell<M>(rhs, cell, sb.UB, sb.par);
+    const P4 rp = p4(sb.par), cp = p4(sb.cp[0]);
+    proj_coeffs<M>(rp, cp, sb.c[1]);
     __syncwarp();
+    double pr[T];
+    project_apply<M>(tab, sb.UB, sb.Y1, sb.Y2, sb.c[1], pass_mask(rp, cp), pr);
+#pragma unroll
+    for (int t = 0; t < T; ++t) R[t] -= pr[t];
   }
   // apply_update: f += dt*delta; grad_normalize; retry at dt/2 on NonphysicalState
   for (int attempt = 0; attempt < 2; ++attempt) {
     const double step = attempt == 0 ? dt : 0.5 * dt;
-    for (int k = lane; k < Cfg<M>::N; k += 32) sb.A[k] = fma(step, sb.R[k], sb.S[k]);
-    if (lane < 4) sb.par[lane] = sb.cp[lane];
+    double v[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) v[t] = fma(step, R[t], sb.cell[0][item_pos<M>(t)]);
     __syncwarp();
-    w = grad_normalize_smem<M>(alpha, sb.A, sb.A2, sb.par, bad);
+    store_items<M>(sb.X1, v);
+    if (lane < 4) sb.par[lane] = sb.cp[0][lane];
+    __syncwarp();
+    const double* res;
+    w = grad_normalize<M, ORDER>(tab, sb, sb.X1, sb.X2, sb.Y1, sb.par, v, bad, &res);
     if (w == W_NONE) {
-      store_cell<M>(f, cell, sb.A, sb.par);
+      store_cell_regs<M>(f, cell, v, sb.par);
+      __syncwarp();
       return W_NONE;
     }
     if (code_of(w) != E_NONPHYSICAL) return w;  // plain Error propagates

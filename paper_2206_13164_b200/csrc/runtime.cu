@@ -17,6 +17,7 @@
 #include "momg_cell.cuh"
 #include "runtime.h"
 #include "sweep_persistent.cuh"
+#include "kernels_v3.cuh"
 
 namespace momg_gpu {
 
@@ -312,6 +313,45 @@ bool persistent_sweep_enabled() {
 }
 void set_sweep_mode(int m) { g_sweep_mode = m; }
 
+// Segment plan of the thread-granular persistent sweep (kernels_v3.cuh):
+// diag_lo[d] and the prefix count of 16-cell segments per anti-diagonal,
+// cached per field; counters shared with the warp-granular sweep.
+tc::SegPlan tc_seg_plan(momg_field* f) {
+  const int nd = f->nx + f->ny - 1;
+  if (!f->seg_plan) {
+    std::vector<int> h(2 * nd + 1);
+    int acc = 0;
+    for (int d = 0; d < nd; ++d) {
+      const int lo = d - (f->ny - 1) > 0 ? d - (f->ny - 1) : 0;
+      const int hi = d < f->nx - 1 ? d : f->nx - 1;
+      h[d] = lo;
+      h[nd + d] = acc;
+      acc += (hi - lo + 1 + tc::SEG - 1) / tc::SEG;
+    }
+    h[2 * nd] = acc;
+    cudaMalloc(&f->seg_plan, h.size() * sizeof(int));
+    cudaMemcpy(f->seg_plan, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
+  }
+  if (!f->sweep_ver) cudaMalloc(&f->sweep_ver, (size_t)f->nx * f->ny * sizeof(unsigned));
+  cudaMemsetAsync(f->sweep_ver, 0, (size_t)f->nx * f->ny * sizeof(unsigned), momg_rt::stream());
+  tc::SegPlan p;
+  p.diag_lo = f->seg_plan;
+  p.seg_start = f->seg_plan + nd;
+  p.ver = f->sweep_ver;
+  p.nd = nd;
+  p.nsweeps = 4;
+  for (int s = 0; s < 8; ++s) p.dirs[s] = s & 3;
+  return p;
+}
+
+int tc_sweep_blocks(const void* kernel, size_t smem) {
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, tc::VS, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms;
+}
+
 // Diagonal-major visiting order of direction (i+, j+) (ii | jj << 16) and the
 // per-cell counters of the persistent sweep, cached per field.
 SweepScratch sweep_scratch(momg_field* f) {
@@ -443,6 +483,7 @@ void field_free(momg_field* f) {
   cudaFree(f->p);
   cudaFree(f->dgrid);
   cudaFree(f->sweep_order);
+  cudaFree(f->seg_plan);
   cudaFree(f->sweep_ver);
   delete f;
 }

@@ -19,6 +19,7 @@ struct momg_field {
   double* dgrid = nullptr;  // dx | dy | xc | yc
   uint32_t* sweep_order = nullptr;  // persistent sweep: diagonal order (lazy)
   unsigned* sweep_ver = nullptr;    // persistent sweep: per-cell counters (lazy)
+  int* seg_plan = nullptr;          // thread-granular sweep: diag_lo | seg_start (lazy)
   DevField dev() const {
     DevField d;
     d.nx = nx;

@@ -50,18 +50,18 @@ struct SweepPlan {
   int dirs[8];            // direction index per sweep (mod 8)
 };
 
-template <int M>
+template <int M, int ORDER>
 __global__ void __launch_bounds__(PWPB * 32) k_sweep_persistent(DevField f, DevField rhs,
                                                                 int has_rhs, DevCtx ctx,
                                                                 DevErr* err, SweepPlan plan) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const BlockView bv = block_setup<M>(smem_raw, &ctx, &f, &rhs, nullptr, nullptr);
-  WarpBuf<M>& sb = warp_buf<M>(bv);
+  const BlockView bv = block_setup<M, ORDER>(smem_raw, &ctx, &f, &rhs, nullptr, nullptr);
+  WarpBuf<M, ORDER>& sb = warp_buf<M, ORDER>(bv);
   const int lane = lane_id();
   const long long cells = (long long)f.nx * f.ny;
   const long long total = cells * plan.nsweeps;
   const long long W = (long long)gridDim.x * PWPB;
-  const int radius = ctx.order == 2 ? 2 : 1;
+  constexpr int radius = ORDER == 2 ? 2 : 1;
   for (long long item = blockIdx.x * (long long)PWPB + (threadIdx.x >> 5); item < total; item += W) {
     const int s = (int)(item / cells);
     const uint32_t packed = plan.order[item - (long long)s * cells];
@@ -89,7 +89,6 @@ __global__ void __launch_bounds__(PWPB * 32) k_sweep_persistent(DevField f, DevF
         need = (unsigned)s + (before ? 1u : 0u);
       }
     }
-    // every lane acquires every dependency (broadcast loads)
     bool ready = false;
     while (!ready) {
       bool mine = dn < 0 || ld_acquire(plan.ver + dn) >= need;
@@ -103,8 +102,9 @@ __global__ void __launch_bounds__(PWPB * 32) k_sweep_persistent(DevField f, DevF
     // barrier orders every lane's following loads after all of them.
     __syncwarp();
     double bad = 0.0;
-    const int w = sweep_cell_smem<M>(&bv.hdr->f, has_rhs ? &bv.hdr->g : nullptr, &bv.hdr->ctx,
-                                     bv.alpha, i, j, sb, &bad);
+    load_stencil<M, ORDER>(&bv.hdr->f, i, j, sb);
+    const int w = sweep_cell<M, ORDER>(&bv.hdr->f, has_rhs ? &bv.hdr->g : nullptr, &bv.hdr->ctx,
+                                       bv.tab, i, j, sb, &bad);
     if (w) {
       if (lane == 0) raise_err(err, code_of(w), w, i, j, bad);
       return;
@@ -123,16 +123,16 @@ struct SweepScratch {
 };
 SweepScratch sweep_scratch(momg_field* f);
 
-template <int M>
+template <int M, int ORDER>
 struct PersistentSweep {
-  static size_t smem() { return BlockSmem<M>::bytes(PWPB); }
+  static size_t smem() { return BlockSmem<M, ORDER>::bytes(PWPB); }
   static int blocks() {
     static int nb = 0;
     if (nb) return nb;
-    cudaFuncSetAttribute(k_sweep_persistent<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_sweep_persistent<M, ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem());
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_persistent<M>, PWPB * 32, smem());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_persistent<M, ORDER>, PWPB * 32, smem());
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     nb = per_sm * sms;
@@ -158,7 +158,7 @@ struct PersistentSweep {
     DevErr* err = momg_rt::err_dev();
     DevCtx c = ctx;
     void* args[] = {&fd, &rd, &has_rhs, &c, &err, &plan};
-    cudaLaunchCooperativeKernel((void*)k_sweep_persistent<M>, dim3(nb), dim3(PWPB * 32), args,
+    cudaLaunchCooperativeKernel((void*)k_sweep_persistent<M, ORDER>, dim3(nb), dim3(PWPB * 32), args,
                                 smem(), momg_rt::stream());
     momg_rt::count_launch(1);
   }

@@ -1,0 +1,164 @@
+"""Generates paper_2206_13164_b200/csrc/gen/simplex_gen.cuh: straight-line
+FP64 code for the multi-index operations of the moment method, one
+specialisation per moment order M.
+
+Every operation of the hot path that mixes coefficients walks a chain along
+one velocity axis of the graded-lex simplex {|alpha| <= M}
+(multi_index.hpp:31-52).  Emitting those chains with compile-time positions
+turns each term into one shared-memory load with an immediate offset plus
+one FMA: no index arithmetic, no tables, no predication at run time.
+
+A thread's vector lives in shared memory at v[k * VS] (VS = threads per
+block, so the vectors of consecutive threads interleave and every access is
+bank-conflict free).
+
+Generated per M (struct Gen<M>):
+  pass<d>(v, c)        in-place axis-d Toeplitz pass g_a = sum_n c_n f_{a - n e_d}
+                       (one factor of the projection; see momg_device.cuh)
+  half_sum<a>(L, R, Ku, Kl)
+                       in place into L: out(beta) = sum_m L(beta|m) Ku[m][p] + R(beta|m) Kl[m][p]
+                       (flux.cpp:58-73 with folded kernels), p = beta_a
+  half_one<a>(L, K)    single-sided variant (wall outgoing flux)
+  full_flux<a>(src, dst, un, th)
+                       flux.cpp:10-27
+Usage: python tools/gen_simplex.py  (writes the header; run by csrc/Makefile)
+"""
+import os
+import sys
+
+ORDERS = [3, 4, 5, 6, 7, 8]
+
+
+def simplex(M):
+    idx = []
+    for deg in range(M + 1):
+        for a1 in range(deg, -1, -1):
+            for a2 in range(deg - a1, -1, -1):
+                idx.append((a1, a2, deg - a1 - a2))
+    return idx
+
+
+def emit_order(M):
+    idx = simplex(M)
+    pos = {a: k for k, a in enumerate(idx)}
+    N = len(idx)
+    L = []
+    w = L.append
+    w(f"template <>\nstruct Gen<{M}> {{")
+    w(f"  static constexpr int N = {N};")
+    # ---------------------------------------------------------------- passes
+    for d in range(3):
+        w(f"  // axis-{d} Toeplitz pass, in place (pencils along axis {d})")
+        w(f"  template <int VS>")
+        w(f"  static __device__ __forceinline__ void pass{d}(double* __restrict__ v, const double* c) {{")
+        others = [o for o in range(3) if o != d]
+        pencils = {}
+        for a in idx:
+            key = (a[others[0]], a[others[1]])
+            pencils.setdefault(key, []).append(a)
+        for key, members in pencils.items():
+            members.sort(key=lambda a: a[d])
+            if len(members) < 2:
+                continue
+            ks = [pos[a] for a in members]
+            w("    {")
+            for j, k in enumerate(ks):
+                w(f"      const double f{j} = v[{k} * VS];")
+            for j in range(len(ks) - 1, 0, -1):
+                expr = f"f{j}"
+                for n in range(1, j + 1):
+                    expr = f"fma(c[{n}], f{j - n}, {expr})"
+                w(f"      v[{ks[j]} * VS] = {expr};")
+            w("    }")
+        w("  }")
+    # ------------------------------------------------------------- half sums
+    for a in range(2):
+        for single in (False, True):
+            name = f"half_one{a}" if single else f"half_sum{a}"
+            args = "double* __restrict__ Lv, const double (&Ku)[%d][%d]" % (M + 1, M + 1) if single else \
+                "double* __restrict__ Lv, const double* __restrict__ Rv, const double (&Ku)[%d][%d], const double (&Kl)[%d][%d]" % (M + 1, M + 1, M + 1, M + 1)
+            w(f"  // half-space flux sum along axis {a}{' (single side)' if single else ''}, in place into Lv")
+            w(f"  template <int VS>")
+            w(f"  static __device__ __forceinline__ void {name}({args}) {{")
+            tans = {}
+            for b in idx:
+                t = tuple(b[o] for o in range(3) if o != a)
+                tans.setdefault(t, []).append(b)
+            for t, members in tans.items():
+                members.sort(key=lambda b: b[a])
+                ks = [pos[b] for b in members]
+                n = len(ks)  # m = 0 .. n-1 (= M - |beta_t|)
+                w("    {")
+                for m, k in enumerate(ks):
+                    w(f"      const double l{m} = Lv[{k} * VS];")
+                    if not single:
+                        w(f"      const double r{m} = Rv[{k} * VS];")
+                for p, k in enumerate(ks):
+                    expr = "0.0"
+                    for m in range(n):
+                        expr = f"fma(l{m}, Ku[{m}][{p}], {expr})" if expr != "0.0" else f"l{m} * Ku[{m}][{p}]"
+                        if not single:
+                            expr = f"fma(r{m}, Kl[{m}][{p}], {expr})"
+                    w(f"      Lv[{k} * VS] = {expr};")
+                w("    }")
+            w("  }")
+    # ------------------------------------------------------------ full flux
+    for a in range(2):
+        w(f"  // full-space flux xi_{a} f (flux.cpp:10-27), closure drops degree M+1")
+        w(f"  template <int VS>")
+        w(f"  static __device__ __forceinline__ void full_flux{a}(const double* __restrict__ s, double* __restrict__ o, double un, double th) {{")
+        for b in idx:
+            k = pos[b]
+            expr = f"un * s[{k} * VS]"
+            if b[a] >= 1:
+                dn = list(b); dn[a] -= 1
+                expr = f"fma(th, s[{pos[tuple(dn)]} * VS], {expr})"
+            if sum(b) < M:
+                up = list(b); up[a] += 1
+                expr = f"fma({float(b[a] + 1)}, s[{pos[tuple(up)]} * VS], {expr})"
+            w(f"    o[{k} * VS] = {expr};")
+        w("  }")
+    # Shakhov eq pattern: positions of 2 e_dd + e_d and the q components
+    w("  // Shakhov equilibrium positions (collision.hpp:95-111): 3 e_d and e_d + 2 e_dd")
+    sh = []
+    for d in range(3):
+        for dd in range(3):
+            b = [0, 0, 0]; b[dd] += 2; b[d] += 1
+            sh.append((pos[tuple(b)], d))
+    w("  static constexpr int SHK[9] = {" + ", ".join(str(k) for k, _ in sh) + "};")
+    w("  static constexpr int SHD[9] = {" + ", ".join(str(d) for _, d in sh) + "};")
+    # degrees and factorials for norms
+    import math
+    w("  static constexpr int DEG[" + str(N) + "] = {" + ", ".join(str(sum(b)) for b in idx) + "};")
+    w("  static constexpr double FACT[" + str(N) + "] = {" + ", ".join(
+        repr(float(math.factorial(b[0]) * math.factorial(b[1]) * math.factorial(b[2]))) for b in idx) + "};")
+    # beta = p e_a positions (in_unit of the wall flux)
+    for a in range(2):
+        ps = []
+        for p in range(M + 1):
+            b = [0, 0, 0]; b[a] = p
+            ps.append(pos[tuple(b)])
+        w(f"  static constexpr int AXP{a}[{M + 1}] = {{" + ", ".join(map(str, ps)) + "};")
+    w("};")
+    return "\n".join(L)
+
+
+def main():
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2206_13164_b200", "csrc", "gen", "simplex_gen.cuh")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    body = ["// GENERATED by tools/gen_simplex.py -- do not edit.",
+            "// Straight-line multi-index operations per moment order (see the generator's docstring).",
+            "#pragma once", "", "namespace momg_gpu {", "", "template <int M>", "struct Gen;", ""]
+    for M in ORDERS:
+        body.append(emit_order(M))
+        body.append("")
+    body.append("}  // namespace momg_gpu")
+    text = "\n".join(body) + "\n"
+    if not os.path.exists(out) or open(out).read() != text:
+        open(out, "w").write(text)
+    print(out, len(text.splitlines()), "lines")
+
+
+if __name__ == "__main__":
+    main()
