@@ -166,6 +166,10 @@ int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_
 int momg_set_sweep_mode(int mode);
 
 /* ---- instrumentation --------------------------------------------------- */
+/* debug: %globaltimer stamps of the first cap work items of the split
+   persistent sweep ([item][4]: start, dependencies ready, faces, update) */
+int momg_debug_trace(long long cap);
+long long momg_debug_trace_read(unsigned long long* host, long long n);
 /* number of kernels this library has launched since load (gpu_launches) */
 long long momg_launch_count(void);
 

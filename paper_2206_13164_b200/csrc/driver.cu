@@ -144,23 +144,29 @@ struct Cycle {
 
 static const int kCanon[4] = {0, 1, 2, 3};
 
+static void sweeps(const momg_gpu::DevCtx& ctx, momg_field* field, const momg_field* rhs, int n) {
+  while (n > 0) {
+    const int k = n < 4 ? n : 4;
+    momg_gpu::op_sweep_n(ctx, field, rhs, kCanon, k);
+    n -= k;
+  }
+}
+
 // nmg_cycle, multigrid.cpp:166-200 (Alg. 2 of the paper).  Device errors are
 // recorded and every later kernel early-exits, so the check is deferred to
 // the caller (solve_steady checks once per outer iteration).
 static void nmg_cycle(Hierarchy& h, int level, momg_field* field, const momg_field* rhs,
                       const momg_gpu::DevCtx& ctx, const Cycle& pol, long long* work) {
   const long long cells = (long long)field->nx * field->ny;
+  // consecutive fast_sweep_step calls run as one overlapped launch (same
+  // results: the per-cell dependency rule is exact across iterations)
   if (level == 0) {
-    for (int s = 0; s < pol.s3; ++s) {
-      momg_gpu::op_sweep(ctx, field, rhs, kCanon);
-      *work += 4 * cells;
-    }
+    sweeps(ctx, field, rhs, pol.s3);
+    *work += 4 * cells * pol.s3;
     return;
   }
-  for (int s = 0; s < pol.s1; ++s) {
-    momg_gpu::op_sweep(ctx, field, rhs, kCanon);
-    *work += 4 * cells;
-  }
+  sweeps(ctx, field, rhs, pol.s1);
+  *work += 4 * cells * pol.s1;
   LevelWork& w = h.work[level];
   momg_gpu::op_residual(ctx, field, w.res.f);
   momg_gpu::op_defect(w.res.f, rhs, w.defect.f);
@@ -171,10 +177,8 @@ static void nmg_cycle(Hierarchy& h, int level, momg_field* field, const momg_fie
   momg_gpu::op_axpy(w.crhs.f, w.cres.f);
   for (int g = 0; g < pol.gamma; ++g) nmg_cycle(h, level - 1, w.coarse.f, w.crhs.f, ctx, pol, work);
   momg_gpu::op_fas(field, w.before.f, w.coarse.f);
-  for (int s = 0; s < pol.s2; ++s) {
-    momg_gpu::op_sweep(ctx, field, rhs, kCanon);
-    *work += 4 * cells;
-  }
+  sweeps(ctx, field, rhs, pol.s2);
+  *work += 4 * cells * pol.s2;
 }
 
 static double scalar(momg_err& e) {

@@ -20,6 +20,7 @@
 #include "runtime.h"
 #include "sweep_persistent.cuh"
 #include "kernels_v3.cuh"
+#include "split_cell.cuh"
 
 namespace momg_gpu {
 
@@ -346,8 +347,13 @@ inline void set_smem(K kernel, size_t bytes) {
 template <int M>
 constexpr bool use_tc() { return M <= 6; }
 
-int tc_sweep_blocks(const void* kernel, size_t smem);
-tc::SegPlan tc_seg_plan(momg_field* f);
+int tc_sweep_blocks(const void* kernel, size_t smem, int threads = tc::VS);
+tc::SegPlan tc_seg_plan(momg_field* f, int seg = tc::SEG);
+template <int M>
+constexpr bool use_split() { return M <= 5; }
+bool split_sweep_enabled();
+unsigned long long* trace_buffer(long long* cap);
+const uint32_t* split_schedule(momg_field* f, int nsweeps, const int* dirs, int radius, int seg);
 
 // ---------------------------------------------------- templated launchers
 template <int M>
@@ -412,6 +418,23 @@ struct Launch {
     momg_rt::count_launch(1);
   }
   static void sweep(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int* order) {
+    sweep_n(ctx, f, rhs, order, 1);
+  }
+  // `iters` consecutive fast_sweep_step calls (identical results; the split
+  // persistent kernel runs them as one launch so the sweeps overlap)
+  static void sweep_n(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int* order, int iters) {
+    if constexpr (use_split<M>()) {
+      if (!(persistent_sweep_enabled() && split_sweep_enabled()) || iters > 4) {
+        for (int it = 0; it < iters; ++it) sweep1(ctx, f, rhs, order, 1);
+        return;
+      }
+    } else {
+      for (int it = 0; it < iters; ++it) sweep1(ctx, f, rhs, order, 1);
+      return;
+    }
+    sweep1(ctx, f, rhs, order, iters);
+  }
+  static void sweep1(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int* order, int iters) {
     if constexpr (use_tc<M>()) {
       tc_attrs();
       const DevField fd = f->dev();
@@ -419,6 +442,34 @@ struct Launch {
       int has_rhs = rhs != nullptr;
       DevErr* err = momg_rt::err_dev();
       DevCtx c = ctx;
+      if constexpr (use_split<M>()) {
+        if (persistent_sweep_enabled() && split_sweep_enabled()) {
+          static bool sattr = false;
+          if (!sattr) {
+            set_smem(sp::k4_sweep<M, 1>, sp::Layout<M>::bytes);
+            set_smem(sp::k4_sweep<M, 2>, sp::Layout<M>::bytes);
+            sattr = true;
+          }
+          const tc::SegPlan p16 = tc_seg_plan(f, 32);
+          sp::SegPlan32 plan;
+          plan.diag_lo = p16.diag_lo;
+          plan.seg_start = p16.seg_start;
+          plan.ver = p16.ver;
+          plan.nd = p16.nd;
+          plan.nsweeps = 4 * iters;
+          for (int s = 0; s < 16; ++s) plan.dirs[s] = order[s & 3];
+          plan.items = split_schedule(f, plan.nsweeps, plan.dirs, ctx.order == 2 ? 2 : 1, 32);
+          plan.trace = trace_buffer(&plan.trace_cap);
+          const void* kern = ctx.order == 2 ? (const void*)sp::k4_sweep<M, 2> : (const void*)sp::k4_sweep<M, 1>;
+          int nb = tc_sweep_blocks(kern, sp::Layout<M>::bytes, sp::THREADS);
+          DevField fa = fd, ra = rd;
+          void* args[] = {&fa, &ra, &has_rhs, &c, &err, &plan};
+          cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(sp::THREADS), args, sp::Layout<M>::bytes,
+                                      momg_rt::stream());
+          momg_rt::count_launch(1);
+          return;
+        }
+      }
       if (persistent_sweep_enabled()) {
         tc::SegPlan plan = tc_seg_plan(f);
         plan.nsweeps = 4;
@@ -542,7 +593,7 @@ struct Launch {
     momg_rt::count_launch(1);
   }
   static const Ops* ops() {
-    static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial};
+    static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial, sweep_n};
     return &o;
   }
 };

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(VS) k3_sweep(DevField f, DevField rhs, int has
       const int axis = tid >> 5, side = (tid >> 4) & 1;
       const int c = j * f.nx + i;
       bool ok = false;
+      long long polls = 0;
       while (!ok) {
         ok = true;
         if (axis == 0 && side == 0 && ld_acquire(plan.ver + c) < (unsigned)s) ok = false;
@@ -201,6 +202,10 @@ __global__ void __launch_bounds__(VS) k3_sweep(DevField f, DevField rhs, int has
         }
         if (!ok) {
           if (err_on(err)) break;
+          if (++polls > (1LL << 26)) {  // deadlock guard: fail loudly, never hang
+            raise(err, E_ERROR, W_DEADLOCK, i, j, (double)s);
+            break;
+          }
           __nanosleep(64);
         }
       }

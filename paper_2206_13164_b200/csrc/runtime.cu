@@ -4,6 +4,7 @@
 // driver.cu.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -211,6 +212,7 @@ static const char* what_text(int w) {
     case W_FAS: return "coarse-grid correction left cell nonphysical";
     case W_RESTRICT: return "restrict_solution: nonphysical coarse state";
     case W_ES_UNSUPPORTED: return "ES-BGK collision is not available on the device path";
+    case W_DEADLOCK: return "persistent sweep: dependency wait timed out (internal error)";
     default: return "unknown failure";
   }
 }
@@ -312,13 +314,17 @@ bool persistent_sweep_enabled() {
   return g_sweep_mode == 1;
 }
 void set_sweep_mode(int m) { g_sweep_mode = m; }
+void set_split_mode(int m);
+void set_trace(long long cap);
+long long read_trace(unsigned long long* host, long long n);
 
 // Segment plan of the thread-granular persistent sweep (kernels_v3.cuh):
 // diag_lo[d] and the prefix count of 16-cell segments per anti-diagonal,
 // cached per field; counters shared with the warp-granular sweep.
-tc::SegPlan tc_seg_plan(momg_field* f) {
+tc::SegPlan tc_seg_plan(momg_field* f, int seg) {
   const int nd = f->nx + f->ny - 1;
-  if (!f->seg_plan) {
+  int*& plan_ptr = seg == 32 ? f->seg_plan32 : f->seg_plan;
+  if (!plan_ptr) {
     std::vector<int> h(2 * nd + 1);
     int acc = 0;
     for (int d = 0; d < nd; ++d) {
@@ -326,17 +332,17 @@ tc::SegPlan tc_seg_plan(momg_field* f) {
       const int hi = d < f->nx - 1 ? d : f->nx - 1;
       h[d] = lo;
       h[nd + d] = acc;
-      acc += (hi - lo + 1 + tc::SEG - 1) / tc::SEG;
+      acc += (hi - lo + 1 + seg - 1) / seg;
     }
     h[2 * nd] = acc;
-    cudaMalloc(&f->seg_plan, h.size() * sizeof(int));
-    cudaMemcpy(f->seg_plan, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMalloc(&plan_ptr, h.size() * sizeof(int));
+    cudaMemcpy(plan_ptr, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
   }
   if (!f->sweep_ver) cudaMalloc(&f->sweep_ver, (size_t)f->nx * f->ny * sizeof(unsigned));
   cudaMemsetAsync(f->sweep_ver, 0, (size_t)f->nx * f->ny * sizeof(unsigned), momg_rt::stream());
   tc::SegPlan p;
-  p.diag_lo = f->seg_plan;
-  p.seg_start = f->seg_plan + nd;
+  p.diag_lo = plan_ptr;
+  p.seg_start = plan_ptr + nd;
   p.ver = f->sweep_ver;
   p.nd = nd;
   p.nsweeps = 4;
@@ -344,9 +350,128 @@ tc::SegPlan tc_seg_plan(momg_field* f) {
   return p;
 }
 
-int tc_sweep_blocks(const void* kernel, size_t smem) {
+}  // namespace momg_gpu
+
+// Dependency-level schedule of the split persistent sweep: work item = (sweep
+// s, anti-diagonal d, 32-cell segment).  level(item) = 1 + max level of the
+// items owning its cells' dependencies (the rule of sweep_persistent.cuh);
+// items sorted by (level, sweep-major index) form a topological order in
+// which sweep s+1 starts as soon as sweep s has passed its first cells.
+struct Schedule {
+  int nsweeps = 0, radius = 0, seg = 0;
+  int dirs[16] = {0};
+  uint32_t* dev = nullptr;
+};
+
+namespace momg_gpu {
+
+const uint32_t* split_schedule(momg_field* f, int nsweeps, const int* dirs, int radius, int seg) {
+  Schedule*& sc = f->schedule;
+  if (sc && sc->nsweeps == nsweeps && sc->radius == radius && sc->seg == seg &&
+      std::equal(dirs, dirs + nsweeps, sc->dirs))
+    return sc->dev;
+  if (!sc) sc = new Schedule();
+  if (sc->dev) cudaFree(sc->dev);
+  sc->nsweeps = nsweeps;
+  sc->radius = radius;
+  sc->seg = seg;
+  std::copy(dirs, dirs + nsweeps, sc->dirs);
+  const int nx = f->nx, ny = f->ny, nd = nx + ny - 1;
+  std::vector<int> dlo(nd), sstart(nd + 1);
+  int acc = 0;
+  for (int d = 0; d < nd; ++d) {
+    const int lo = d - (ny - 1) > 0 ? d - (ny - 1) : 0;
+    const int hi = d < nx - 1 ? d : nx - 1;
+    dlo[d] = lo;
+    sstart[d] = acc;
+    acc += (hi - lo + 1 + seg - 1) / seg;
+  }
+  sstart[nd] = acc;
+  const int per = acc;
+  auto item_of = [&](int s, int i, int j) {
+    const int dir = dirs[s];
+    const bool iu = dir == 0 || dir == 3, ju = dir == 0 || dir == 1;
+    const int ii = iu ? i : nx - 1 - i, jj = ju ? j : ny - 1 - j;
+    const int d = ii + jj;
+    return s * per + sstart[d] + (ii - dlo[d]) / seg;
+  };
+  std::vector<int> level((size_t)per * nsweeps, 0);
+  for (int s = 0; s < nsweeps; ++s) {
+    const int dir = dirs[s];
+    const bool iu = dir == 0 || dir == 3, ju = dir == 0 || dir == 1;
+    for (int d = 0; d < nd; ++d) {
+      const int hi = d < nx - 1 ? d : nx - 1;
+      for (int sg = 0; sstart[d] + sg < sstart[d + 1]; ++sg) {
+        const int id = s * per + sstart[d] + sg;
+        int lv = 0;
+        for (int ii = dlo[d] + sg * seg; ii <= hi && ii < dlo[d] + (sg + 1) * seg; ++ii) {
+          const int jj = d - ii;
+          const int i = iu ? ii : nx - 1 - ii, j = ju ? jj : ny - 1 - jj;
+          if (s > 0) lv = std::max(lv, level[item_of(s - 1, i, j)] + 1);
+          for (int dist = 1; dist <= radius; ++dist) {
+            const int nb[4][2] = {{i - dist, j}, {i + dist, j}, {i, j - dist}, {i, j + dist}};
+            for (int q = 0; q < 4; ++q) {
+              const int ni = nb[q][0], nj = nb[q][1];
+              if (ni < 0 || ni >= nx || nj < 0 || nj >= ny) continue;
+              const bool before = q < 2 ? (iu ? ni < i : ni > i) : (ju ? nj < j : nj > j);
+              if (before) lv = std::max(lv, level[item_of(s, ni, nj)] + 1);
+              else if (s > 0) lv = std::max(lv, level[item_of(s - 1, ni, nj)] + 1);
+            }
+          }
+        }
+        level[id] = lv;
+      }
+    }
+  }
+  std::vector<int> ids((size_t)per * nsweeps);
+  for (size_t k = 0; k < ids.size(); ++k) ids[k] = (int)k;
+  std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) { return level[a] < level[b]; });
+  std::vector<uint32_t> packed(ids.size());
+  for (size_t k = 0; k < ids.size(); ++k) {
+    const int s = ids[k] / per, r = ids[k] % per;
+    const int d = (int)(std::upper_bound(sstart.begin(), sstart.end(), r) - sstart.begin()) - 1;
+    packed[k] = ((uint32_t)s << 28) | ((uint32_t)(r - sstart[d]) << 16) | (uint32_t)d;
+  }
+  cudaMalloc(&sc->dev, packed.size() * sizeof(uint32_t));
+  cudaMemcpy(sc->dev, packed.data(), packed.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  return sc->dev;
+}
+
+static unsigned long long* g_trace = nullptr;
+static long long g_trace_cap = 0;
+unsigned long long* trace_buffer(long long* cap) {
+  *cap = g_trace_cap;
+  return g_trace;
+}
+void set_trace(long long cap) {
+  if (g_trace) cudaFree(g_trace);
+  g_trace = nullptr;
+  g_trace_cap = 0;
+  if (cap > 0 && cudaMalloc(&g_trace, cap * 8 * sizeof(unsigned long long)) == cudaSuccess) {
+    cudaMemset(g_trace, 0, cap * 8 * sizeof(unsigned long long));
+    g_trace_cap = cap;
+  }
+}
+long long read_trace(unsigned long long* host, long long n) {
+  if (!g_trace) return 0;
+  if (n > g_trace_cap) n = g_trace_cap;
+  cudaMemcpy(host, g_trace, n * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return n;
+}
+
+static int g_split = -1;
+bool split_sweep_enabled() {
+  if (g_split < 0) {
+    const char* e = std::getenv("MOMG_SPLIT");
+    g_split = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  return g_split == 1;
+}
+void set_split_mode(int m) { g_split = m; }
+
+int tc_sweep_blocks(const void* kernel, size_t smem, int threads) {
   int per_sm = 0, dev = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, tc::VS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return per_sm * sms;
@@ -377,6 +502,9 @@ void op_residual(const DevCtx& ctx, const momg_field* f, momg_field* out) {
 }
 void op_sweep(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int order[4]) {
   ops_for(f->M)->sweep(ctx, f, rhs, order);
+}
+void op_sweep_n(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int order[4], int iters) {
+  ops_for(f->M)->sweep_n(ctx, f, rhs, order, iters);
 }
 void op_restrict_sol(const momg_field* fine, momg_field* coarse) {
   ops_for(fine->M)->restrict_sol(fine, coarse);
@@ -484,6 +612,11 @@ void field_free(momg_field* f) {
   cudaFree(f->dgrid);
   cudaFree(f->sweep_order);
   cudaFree(f->seg_plan);
+  cudaFree(f->seg_plan32);
+  if (f->schedule) {
+    cudaFree(f->schedule->dev);
+    delete f->schedule;
+  }
   cudaFree(f->sweep_ver);
   delete f;
 }
@@ -532,9 +665,19 @@ int momg_synchronize(momg_err* err) {
 const char* momg_version(void) { return "momg_gpu 0.1 (sm_100a, FP64)"; }
 int momg_supported_order(int M) { return momg_gpu::supported(M) ? 1 : 0; }
 long long momg_launch_count(void) { return momg_rt::launches(); }
+// Debug instrumentation of the split persistent sweep: per-item %globaltimer
+// stamps (start, deps ready, faces done, update done) for the first `cap` items.
+int momg_debug_trace(long long cap) {
+  momg_gpu::set_trace(cap);
+  return MOMG_OK;
+}
+long long momg_debug_trace_read(unsigned long long* host, long long n) {
+  return momg_gpu::read_trace(host, n);
+}
 int momg_set_sweep_mode(int mode) {
-  if (mode != 0 && mode != 1) return MOMG_ERR_ARG;
-  momg_gpu::set_sweep_mode(mode);
+  if (mode < 0 || mode > 2) return MOMG_ERR_ARG;
+  momg_gpu::set_sweep_mode(mode == 0 ? 0 : 1);
+  momg_gpu::set_split_mode(mode == 2 ? 0 : 1);
   return MOMG_OK;
 }
 

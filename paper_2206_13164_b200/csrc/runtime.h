@@ -20,6 +20,8 @@ struct momg_field {
   uint32_t* sweep_order = nullptr;  // persistent sweep: diagonal order (lazy)
   unsigned* sweep_ver = nullptr;    // persistent sweep: per-cell counters (lazy)
   int* seg_plan = nullptr;          // thread-granular sweep: diag_lo | seg_start (lazy)
+  int* seg_plan32 = nullptr;        // split sweep (32-cell segments)
+  struct Schedule* schedule = nullptr;  // split sweep: cached dependency-level item order
   DevField dev() const {
     DevField d;
     d.nx = nx;
@@ -55,6 +57,7 @@ struct Ops {
   void (*fas)(momg_field*, const momg_field*, const momg_field*);
   void (*defect)(const momg_field*, const momg_field*, momg_field*);
   void (*norm_partial)(const momg_field*, const momg_field*, double*, int);
+  void (*sweep_n)(const DevCtx&, momg_field*, const momg_field*, const int*, int);
 };
 const Ops* ops_for(int M);
 DevCtx make_ctx(const momg_ctx* c);
@@ -66,6 +69,7 @@ void field_free(momg_field* f);
 // surface at the next sync_check / fetch_scalar.
 void op_residual(const DevCtx& ctx, const momg_field* f, momg_field* out);
 void op_sweep(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int order[4]);
+void op_sweep_n(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int order[4], int iters);
 void op_restrict_sol(const momg_field* fine, momg_field* coarse);
 void op_restrict_res(const momg_field* arrays, const momg_field* coarse, momg_field* out);
 void op_fas(momg_field* fine, const momg_field* before, const momg_field* after);

@@ -1,0 +1,651 @@
+// Split design of the exact-order fast-sweeping update (moment orders 3..5).
+//
+// The sweep is latency-bound: its dependency DAG has ~2.5-4 (nx+ny) levels
+// per iteration, so the time of ONE cell update is what matters.  A block
+// updates a segment of 32 independent cells of one anti-diagonal (lane =
+// cell).  The four face fluxes of every cell are evaluated concurrently by
+// four face groups of 4 warps each, and each face's work (the two
+// projections into the face basis, the half-space flux, the projection back)
+// is cut into 4 compile-time partitions of balanced cost (gen/split_gen.cuh),
+// one per warp.  Axis passes are split by pencils (disjoint element sets) and
+// run in place; a named barrier of the face group separates consecutive
+// passes.  Group 0 then assembles the residual, applies the local update and
+// re-normalises, again split 4 ways.  Control flow around barriers is uniform
+// per group (per-cell decisions only select the work done between barriers).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "gen/split_gen.cuh"
+#include "thread_cell.cuh"
+#include "types.h"
+
+namespace momg_gpu {
+namespace sp {
+
+constexpr int P = 4;                 // warps (partitions) per face group
+constexpr int G = 4;                 // face groups: x-low, x-high, y-low, y-high
+constexpr int THREADS = 32 * P * G;  // 512
+
+using tc::P4;
+
+template <int M>
+struct Layout {
+  static constexpr int N = Gen<M>::N;
+  static constexpr int VEC = N * 32;  // doubles of one vector for the 32 cells
+  static constexpr size_t bytes = (size_t)G * 3 * VEC * sizeof(double) + 64;
+};
+
+// Non-.aligned named barriers: lanes of one warp may reach them from
+// divergent paths (bar.sync is the .aligned form and would not allow it).
+__device__ __forceinline__ void gbar(int g) {
+  asm volatile("barrier.cta.sync %0, %1;" ::"r"(g + 1), "r"(32 * P) : "memory");
+}
+// barrier of face group g returning whether any thread passed a nonzero flag
+__device__ __forceinline__ int gbar_or(int g, int flag) {
+  int out;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.s32 p, %1, 0;\n barrier.cta.red.or.pred q, %2, %3, p;\n"
+      " selp.s32 %0, 1, 0, q;\n}"
+      : "=r"(out)
+      : "r"(flag), "r"(g + 1), "r"(32 * P)
+      : "memory");
+  return out;
+}
+
+#define SP_DISPATCH(q, call) \
+  switch (q) {               \
+    case 0: call(0); break;  \
+    case 1: call(1); break;  \
+    case 2: call(2); break;  \
+    default: call(3); break; \
+  }
+
+// projection coefficients of exp(a t + b t^2) (see tc::project)
+template <int M>
+__device__ __forceinline__ void coeffs(const P4& from, const P4& to, int d, double* c) {
+  const double b2 = -(to.v[3] - from.v[3]);
+  const double a = -(to.v[d] - from.v[d]);
+  c[0] = 1.0;
+  c[1] = a;
+#pragma unroll
+  for (int n = 2; n <= M; ++n) c[n] = fma(a, c[n - 1], b2 * c[n - 2]) * tc::rcp(n);
+}
+
+// one in-place axis pass of partition q on vector v (base of this cell)
+template <int M>
+__device__ __forceinline__ void pass(int q, int d, double* v, const double* c) {
+#define SP_PASS(Q)                                            \
+  {                                                           \
+    if (d == 0) Split<M, P>::pass0_##Q(v, c);                 \
+    else if (d == 1) Split<M, P>::pass1_##Q(v, c);            \
+    else Split<M, P>::pass2_##Q(v, c);                        \
+  }
+  SP_DISPATCH(q, SP_PASS)
+#undef SP_PASS
+}
+
+// Projection (projection.hpp:64-89) of the vectors of this cell, split over
+// the group's partitions: every thread of the group runs the three passes
+// and barriers; `active` selects whether this cell's vector is touched.
+template <int M>
+__device__ __forceinline__ void project2(int g, int q, double* a, const P4& af, const P4& at, bool act_a,
+                                         double* b, const P4& bf, const P4& bt, bool act_b) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double ca[M + 1], cb[M + 1];
+    coeffs<M>(af, at, d, ca);
+    coeffs<M>(bf, bt, d, cb);
+    if (act_a) pass<M>(q, d, a, ca);
+    if (act_b) pass<M>(q, d, b, cb);
+    gbar(g);
+  }
+}
+
+template <int M, int AXIS>
+__device__ __forceinline__ void half_sum(int q, const double* L, const double* U, const double (&Ku)[M + 1][M + 1],
+                                         const double (&Kl)[M + 1][M + 1], double* o) {
+#define SP_HALF(Q)                                                      \
+  {                                                                     \
+    if (AXIS == 0) Split<M, P>::half_sum0_##Q(L, U, Ku, Kl, o);         \
+    else Split<M, P>::half_sum1_##Q(L, U, Ku, Kl, o);                   \
+  }
+  SP_DISPATCH(q, SP_HALF)
+#undef SP_HALF
+}
+template <int M, int AXIS>
+__device__ __forceinline__ void half_one(int q, const double* L, const double (&K)[M + 1][M + 1], double* o) {
+#define SP_ONE(Q)                                            \
+  {                                                          \
+    if (AXIS == 0) Split<M, P>::half_one0_##Q(L, K, o);      \
+    else Split<M, P>::half_one1_##Q(L, K, o);                \
+  }
+  SP_DISPATCH(q, SP_ONE)
+#undef SP_ONE
+}
+template <int M, int AXIS>
+__device__ __forceinline__ void full_flux(int q, const double* s, double* o, double un, double th) {
+#define SP_FULL(Q)                                                 \
+  {                                                                \
+    if (AXIS == 0) Split<M, P>::full_flux0_##Q(s, o, un, th);      \
+    else Split<M, P>::full_flux1_##Q(s, o, un, th);                \
+  }
+  SP_DISPATCH(q, SP_FULL)
+#undef SP_FULL
+}
+
+__device__ __forceinline__ double rep_u32(const double* v, const P4& p, int axis) {
+  return p.v[axis] + v[(1 + axis) * 32] / v[0];
+}
+__device__ __forceinline__ double rep_theta32(const double* v, const P4& p) {
+  const double rho = v[0];
+  double trace = 0.0, fe2 = 0.0;
+  const double c1 = v[1 * 32], c2 = v[2 * 32], c3 = v[3 * 32];
+  trace += v[4 * 32];
+  fe2 += c1 * c1;
+  trace += v[7 * 32];
+  fe2 += c2 * c2;
+  trace += v[9 * 32];
+  fe2 += c3 * c3;
+  return p.v[3] + (2.0 * trace - fe2 / rho) / (3.0 * rho);
+}
+__device__ __forceinline__ double grad_defect32(const double* v) {
+  double defect = 0.0, trace = 0.0;
+  defect = tc::smax(defect, fabs(v[1 * 32]));
+  trace += v[4 * 32];
+  defect = tc::smax(defect, fabs(v[2 * 32]));
+  trace += v[7 * 32];
+  defect = tc::smax(defect, fabs(v[3 * 32]));
+  trace += v[9 * 32];
+  defect = tc::smax(defect, fabs(trace));
+  return defect / fabs(v[0]);
+}
+
+template <int M>
+__device__ __forceinline__ void krange(int q, int* lo, int* hi) {
+  *lo = (q * Gen<M>::N) / P;
+  *hi = ((q + 1) * Gen<M>::N) / P;
+}
+
+enum : int { B_NONE = 0, B_HALF = 1, B_FULL_L = 2, B_FULL_R = 3, B_WALL = 4 };
+
+// Element-wise copies of partition Q with compile-time bounds: every load is
+// issued before the first dependent store, so one L2 round trip covers the
+// whole partition (a runtime-bounded loop serialises them).
+template <int M, int Q>
+struct Part {
+  static constexpr int LO = (Q * Gen<M>::N) / P, HI = ((Q + 1) * Gen<M>::N) / P, CNT = HI - LO;
+  static __device__ __forceinline__ void load(const double* __restrict__ src, double* __restrict__ dst) {
+    double r[CNT];
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) r[k] = __ldcg(src + LO + k);
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) dst[(LO + k) * 32] = r[k];
+  }
+  // dst = c + off * (h - l) * rh  (second-order face state, spatial.cpp:64-80)
+  static __device__ __forceinline__ void recon(const double* __restrict__ c, const double* __restrict__ l,
+                                               const double* __restrict__ h, double off, double rh,
+                                               double* __restrict__ dst) {
+    double rc[CNT], rl[CNT], rhh[CNT];
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) {
+      rc[k] = __ldcg(c + LO + k);
+      rl[k] = __ldcg(l + LO + k);
+      rhh[k] = __ldcg(h + LO + k);
+    }
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) dst[(LO + k) * 32] = fma(off, (rhh[k] - rl[k]) * rh, rc[k]);
+  }
+  // residual assembly (spatial.cpp:127-132, collision.hpp:120-127), update_delta
+  // (single_level.cpp:64-70) and f + dt delta (apply_update :47)
+  static __device__ __forceinline__ void assemble(const double* S, const double* RH, const double* Fxm,
+                                                  const double* Fxp, const double* Fym, const double* Fyp,
+                                                  double nu, int shakhov, double shw, const double* qv,
+                                                  double idx, double idy, double dt, bool rhs, double* D,
+                                                  double* V) {
+#pragma unroll
+    for (int kk = 0; kk < CNT; ++kk) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int k = LO + kk;
+      double eq = k == 0 ? S[0] : 0.0;
+      if (shakhov) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int e = 0; e < 3; ++e)
+            if (k == flat3((e == 0 ? 2 : 0) + (d == 0), (e == 1 ? 2 : 0) + (d == 1), (e == 2 ? 2 : 0) + (d == 2)))
+              eq = shw * qv[d];
+      }
+      const double sk = S[k * 32];
+      double r = nu * (eq - sk);
+      r -= (Fxp[k * 32] - Fxm[k * 32]) * idx;
+      r -= (Fyp[k * 32] - Fym[k * 32]) * idy;
+      if (rhs) r -= RH[k * 32];
+      D[k * 32] = r;
+      V[k * 32] = fma(dt, r, sk);
+    }
+  }
+  static __device__ __forceinline__ void restep(const double* S, const double* D, double step, double* V) {
+#pragma unroll
+    for (int kk = 0; kk < CNT; ++kk) V[(LO + kk) * 32] = fma(step, D[(LO + kk) * 32], S[(LO + kk) * 32]);
+  }
+  static __device__ __forceinline__ void store(const double* __restrict__ v, double* __restrict__ dst) {
+    double r[CNT];
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) r[k] = v[(LO + k) * 32];
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) __stcg(dst + LO + k, r[k]);
+  }
+};
+
+template <int M>
+__device__ __forceinline__ void part_load(int q, const double* src, double* dst) {
+#define SP_LD(Q) Part<M, Q>::load(src, dst)
+  SP_DISPATCH(q, SP_LD)
+#undef SP_LD
+}
+template <int M>
+__device__ __forceinline__ void part_recon(int q, const double* c, const double* l, const double* h, double off,
+                                           double rh, double* dst) {
+#define SP_RC(Q) Part<M, Q>::recon(c, l, h, off, rh, dst)
+  SP_DISPATCH(q, SP_RC)
+#undef SP_RC
+}
+template <int M>
+__device__ __forceinline__ void part_store(int q, const double* v, double* dst) {
+#define SP_ST(Q) Part<M, Q>::store(v, dst)
+  SP_DISPATCH(q, SP_ST)
+#undef SP_ST
+}
+
+// --------------------------------------------------------------- face phase
+// Face flux of face group g (AXIS = g/2, high = g%2) for cell (i, j) (lane),
+// partition q; result (cell basis) left in F.  `valid` false: barriers only.
+// Returns W_NONE or the failure kind (same in all partitions of the cell).
+__device__ __forceinline__ unsigned long long gtimer0() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int M, int ORDER, int AXIS>
+__device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, int g, int q, bool valid,
+                                          int i, int j, double* L, double* U, double* F,
+                                          unsigned long long* stamp = nullptr) {
+  constexpr int NP = (Gen<M>::N + 3) & ~3;
+  const bool high = g & 1;
+  const int n = AXIS == 0 ? f.nx : f.ny;
+  const int pos = AXIS == 0 ? i : j;
+  const size_t cell = (size_t)j * f.nx + i;
+  const size_t stride = AXIS == 0 ? 1 : (size_t)f.nx;
+  int klo, khi;
+  krange<M>(q, &klo, &khi);
+  int branch = B_NONE;
+  int fail = W_NONE;
+  P4 cp{}, lp{}, rp{}, fp{};
+  const double* xc = AXIS == 0 ? f.xc : f.yc;
+  const double* dd = AXIS == 0 ? f.dx : f.dy;
+  // ---- phase 0: face states (spatial.cpp:34-80) into L / U
+  if (valid) {
+    cp = tc::ldp<true>(f.p + cell * 4);
+    const bool at_wall = high ? pos == n - 1 : pos == 0;
+    if (at_wall) {
+      branch = B_WALL;
+      part_load<M>(q, f.c + cell * NP, L);
+    } else {
+      branch = B_HALF;
+      const int pl = high ? pos : pos - 1, pu = pl + 1;
+      const size_t cl = high ? cell : cell - stride, cu = cl + stride;
+      // lower state on its high side, upper state on its low side
+      for (int side = 0; side < 2; ++side) {
+        const int pc = side == 0 ? pl : pu;
+        const size_t cc = side == 0 ? cl : cu;
+        double* dst = side == 0 ? L : U;
+        P4 pr = tc::ldp<true>(f.p + cc * 4);
+        bool recon = false;
+        size_t lo = cc, hi = cc;
+        double off = 0.0, h = 1.0;
+        if (ORDER == 2 && pc > 0 && pc < n - 1) {
+          lo = cc - stride;
+          hi = cc + stride;
+          h = xc[pc + 1] - xc[pc - 1];
+          off = (side == 0 ? 0.5 : -0.5) * dd[pc];
+          const P4 pl4 = tc::ldp<true>(f.p + lo * 4), ph4 = tc::ldp<true>(f.p + hi * 4);
+          P4 w;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) w.v[qq] = pr.v[qq] + off * ((ph4.v[qq] - pl4.v[qq]) / h);
+          if (w.v[3] > 0.0) {
+            recon = true;
+            pr = w;
+          }
+        }
+        const double* sc = f.c + cc * NP;
+        if (recon)
+          part_recon<M>(q, sc, f.c + lo * NP, f.c + hi * NP, off, 1.0 / h, dst);
+        else
+          part_load<M>(q, sc, dst);
+        if (side == 0) lp = pr; else rp = pr;
+      }
+    }
+  }
+  gbar(g);
+  if (stamp) stamp[0] = gtimer0();
+  // ---- phase 1: wave-speed bounds and branch (flux.cpp:77-97)
+  P4 wb{};
+  double rs = 1.0;
+  if (branch == B_WALL) {
+    const int w = AXIS == 0 ? (high ? 1 : 0) : (high ? 3 : 2);
+    wb.v[AXIS == 0 ? 1 : 0] = ctx.wall_speed[w];
+    wb.v[3] = ctx.wall_theta[w];
+    if (!(wb.v[3] > 0.0)) {
+      fail = W_PROJ_SPREAD;
+      branch = B_NONE;
+    } else {
+      rs = sqrt(wb.v[3]);
+    }
+  } else if (branch == B_HALF) {
+    const double ul = rep_u32(L, lp, AXIS), ur = rep_u32(U, rp, AXIS);
+    const double cl = ctx.c_bound * sqrt(rep_theta32(L, lp));
+    const double cr = ctx.c_bound * sqrt(rep_theta32(U, rp));
+    const double lminus = tc::smin(ul - cl, ur - cr);
+    const double lplus = tc::smax(ul + cl, ur + cr);
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) fp.v[qq] = 0.5 * (lp.v[qq] + rp.v[qq]);
+    if (!(fp.v[3] > 0.0)) {
+      fail = W_PROJ_SPREAD;
+      branch = B_NONE;
+    } else if (lminus >= 0.0) {
+      branch = B_FULL_L;
+    } else if (lplus <= 0.0) {
+      branch = B_FULL_R;
+    }
+    rs = fp.v[3] > 0.0 ? sqrt(fp.v[3]) : 1.0;
+  }
+  // ---- phase 2: project the state(s) into the face (or wall) basis
+  {
+    const bool wall = branch == B_WALL;
+    project2<M>(g, q, L, wall ? cp : lp, wall ? wb : fp, wall || branch == B_HALF || branch == B_FULL_L,
+                U, rp, fp, branch == B_HALF || branch == B_FULL_R);
+  }
+  if (stamp) stamp[1] = gtimer0();
+  // ---- phase 3: flux in the face basis into F
+  double Ku[M + 1][M + 1], Kl[M + 1][M + 1];
+  if (branch == B_HALF || branch == B_WALL) {
+    tc::half_kernels<M>(branch == B_WALL ? 0.0 : fp.v[AXIS], rs, Ku, Kl);
+    if (branch == B_HALF) half_sum<M, AXIS>(q, L, U, Ku, Kl, F);
+    else half_one<M, AXIS>(q, L, high ? Ku : Kl, F);
+  } else if (branch == B_FULL_L) {
+    full_flux<M, AXIS>(q, L, F, fp.v[AXIS], fp.v[3]);
+  } else if (branch == B_FULL_R) {
+    full_flux<M, AXIS>(q, U, F, fp.v[AXIS], fp.v[3]);
+  }
+  gbar(g);
+  if (stamp) stamp[2] = gtimer0();
+  // wall closure: density of the incoming wall Maxwellian (flux.cpp:119-129)
+  if (branch == B_WALL && q == 0) {
+    const double in0 = high ? Kl[0][0] : Ku[0][0];
+    const double wall_rho = in0 == 0.0 ? 0.0 : -F[0] / in0;
+    if (in0 == 0.0) {
+      fail = W_WALL_DEGEN;
+    } else if (!(wall_rho > 0.0)) {
+      fail = W_WALL_RHO;
+    } else {
+#pragma unroll
+      for (int p = 1; p <= M; ++p) {
+        const int k = AXIS == 0 ? flat3(p, 0, 0) : flat3(0, p, 0);
+        F[k * 32] = fma(wall_rho, high ? Kl[0][p] : Ku[0][p], F[k * 32]);
+      }
+      F[0] = 0.0;
+    }
+  }
+  gbar(g);
+  // ---- phase 4: flux back into the cell basis (in F)
+  const P4 from = branch == B_WALL ? wb : fp;
+  project2<M>(g, q, F, from, cp, branch != B_NONE, U, cp, cp, false);
+  return fail;
+}
+
+// ------------------------------------------------------------- cell update
+// sweep_cell (single_level.cpp:103-111): local dt, residual assembly
+// (spatial.cpp:127-132), rhs projection (update_delta :64-70), the update and
+// grad_normalize with the dt/2 retry (apply_update :44-62); face group 0.
+template <int M>
+__device__ __forceinline__ int update_split(const DevField& f, const DevField* rhs, const DevCtx& ctx,
+                                            int q, bool valid, int i, int j, double* base, double* bad) {
+  constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, VEC = Layout<M>::VEC;
+  const int c = threadIdx.x & 31;
+  double* S = base + 0 * VEC + c;       // L_0
+  double* RH = base + 1 * VEC + c;      // U_0
+  double* V = base + 3 * VEC + c;       // L_1
+  double* D = base + 4 * VEC + c;       // U_1
+  const double* Fxm = base + 2 * VEC + c;
+  const double* Fxp = base + 5 * VEC + c;
+  const double* Fym = base + 8 * VEC + c;
+  const double* Fyp = base + 11 * VEC + c;
+  int klo, khi;
+  krange<M>(q, &klo, &khi);
+  const size_t cell = (size_t)j * f.nx + i;
+  P4 cp{}, rp{};
+  if (valid) {
+    cp = tc::ldp<true>(f.p + cell * 4);
+    part_load<M>(q, f.c + cell * NP, S);
+    if (rhs) {
+      rp = tc::ldp<true>(rhs->p + cell * 4);
+      part_load<M>(q, rhs->c + cell * NP, RH);
+    }
+  }
+  gbar(0);
+  int fail = W_NONE;
+  double dt = 0.0, nu = 0.0, qv[3] = {0.0, 0.0, 0.0};
+  if (valid) {
+    if (!(cp.v[3] > 0.0)) {
+      fail = W_DT_THETA;
+    } else {
+      const double cc = ctx.cfl_c_bound * sqrt(cp.v[3]);
+      dt = ctx.cfl / ((fabs(cp.v[0]) + cc) / f.dx[i] + (fabs(cp.v[1]) + cc) / f.dy[j]);
+      const double rho = S[0];
+      if (!(rho > 0.0)) fail = W_MACRO_RHO;
+      else if (ctx.collision == 1) fail = W_ES_UNSUPPORTED;
+      else {
+        nu = ctx.nu_coef * rho * pow(cp.v[3], ctx.nu_exp);
+        if (ctx.collision == 2) {
+          qv[0] = 2.0 * S[flat3(3, 0, 0) * 32] + S[flat3(3, 0, 0) * 32] + S[flat3(1, 2, 0) * 32] + S[flat3(1, 0, 2) * 32];
+          qv[1] = 2.0 * S[flat3(0, 3, 0) * 32] + S[flat3(2, 1, 0) * 32] + S[flat3(0, 3, 0) * 32] + S[flat3(0, 1, 2) * 32];
+          qv[2] = 2.0 * S[flat3(0, 0, 3) * 32] + S[flat3(2, 0, 1) * 32] + S[flat3(0, 2, 1) * 32] + S[flat3(0, 0, 3) * 32];
+        }
+      }
+    }
+  }
+  if (rhs) project2<M>(0, q, RH, rp, cp, valid && fail == W_NONE, V, cp, cp, false);
+  const bool ok0 = valid && fail == W_NONE;
+  if (ok0) {
+    const double idx = 1.0 / f.dx[i], idy = 1.0 / f.dy[j];
+    const int shk = ctx.collision == 2;
+    const double shw = ctx.shakhov_w;
+    const bool hr = rhs != nullptr;
+#define SP_AS(Q) Part<M, Q>::assemble(S, RH, Fxm, Fxp, Fym, Fyp, nu, shk, shw, qv, idx, idy, dt, hr, D, V)
+    SP_DISPATCH(q, SP_AS)
+#undef SP_AS
+  }
+  gbar(0);
+  // apply_update with the dt/2 retry; grad_normalize loop uniform per group
+  bool done = !ok0;
+  bool good = false;
+  P4 prm = cp;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    bool active = !done;
+    int status = W_NONE;
+    prm = cp;
+    if (attempt == 1 && active) {
+      const double half = 0.5 * dt;
+#define SP_RS(Q) Part<M, Q>::restep(S, D, half, V)
+      SP_DISPATCH(q, SP_RS)
+#undef SP_RS
+    }
+    gbar(0);
+    for (int iter = 0; iter <= 30; ++iter) {
+      bool need = false;
+      P4 to = prm;
+      if (active) {
+        const double rho = V[0];
+        if (!isfinite(rho) || !(rho > 0.0)) {
+          status = W_GRAD_RHO;
+          *bad = rho;
+          active = false;
+        } else if (grad_defect32(V) <= 1e-12) {
+          active = false;
+        } else if (iter == 30) {
+          status = W_GRAD_CAP;
+          active = false;
+        } else {
+          to.v[0] = rep_u32(V, prm, 0);
+          to.v[1] = rep_u32(V, prm, 1);
+          to.v[2] = rep_u32(V, prm, 2);
+          to.v[3] = rep_theta32(V, prm);
+          if (!isfinite(to.v[3]) || !(to.v[3] > 0.0)) {
+            status = W_GRAD_THETA;
+            *bad = to.v[3];
+            active = false;
+          } else if (!isfinite(to.v[0]) || !isfinite(to.v[1]) || !isfinite(to.v[2])) {
+            status = W_GRAD_U;
+            active = false;
+          } else {
+            need = true;
+          }
+        }
+      }
+      if (!gbar_or(0, need)) break;
+      project2<M>(0, q, V, prm, to, need, D, cp, cp, false);
+      if (need) prm = to;
+    }
+    if (!done) {
+      const bool nonphys = status == W_GRAD_RHO || status == W_GRAD_THETA || status == W_GRAD_U;
+      if (status == W_NONE) {
+        good = true;
+        done = true;
+      } else if (nonphys) {
+        if (attempt == 1) {  // SolverError after the dt/2 retry
+          fail = W_DT_HALVING;
+          done = true;
+        }
+      } else {  // plain Error (iteration cap) propagates
+        fail = status;
+        done = true;
+      }
+    }
+    if (!gbar_or(0, !done)) break;
+  }
+  if (valid && fail == W_NONE && good) {
+    part_store<M>(q, V, f.c + cell * NP);
+    if (q == 0) {
+      __stcg(reinterpret_cast<double2*>(f.p + cell * 4), make_double2(prm.v[0], prm.v[1]));
+      __stcg(reinterpret_cast<double2*>(f.p + cell * 4) + 1, make_double2(prm.v[2], prm.v[3]));
+    }
+    __threadfence();
+  }
+  return (valid && !good && fail == W_NONE) ? W_DT_HALVING : fail;
+}
+
+// ------------------------------------------------ persistent split sweep
+struct SegPlan32 {
+  const int* diag_lo;
+  const int* seg_start;
+  unsigned* ver;
+  const uint32_t* items;  // work items in dependency-level order: s<<28 | seg<<16 | d
+  int nd;
+  int nsweeps;            // <= 16
+  int dirs[16];
+  unsigned long long* trace;  // optional [item][4] %globaltimer stamps (debug)
+  long long trace_cap;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int M, int ORDER>
+__global__ void __launch_bounds__(THREADS, 1) k4_sweep(DevField f, DevField rhs, int has_rhs, DevCtx ctx,
+                                                      DevErr* err, SegPlan32 plan) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int s_stop;
+  constexpr int VEC = Layout<M>::VEC;
+  const int warp = threadIdx.x >> 5, g = warp / P, q = warp % P, c = threadIdx.x & 31;
+  double* L = smem + (g * 3 + 0) * VEC + c;
+  double* U = smem + (g * 3 + 1) * VEC + c;
+  double* F = smem + (g * 3 + 2) * VEC + c;
+  const int per_sweep = plan.seg_start[plan.nd];
+  const long long total = (long long)per_sweep * plan.nsweeps;
+  constexpr int radius = ORDER == 2 ? 2 : 1;
+  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
+    if (threadIdx.x == 0) s_stop = *((volatile const int*)&err->code) != 0;
+    __syncthreads();
+    if (s_stop) return;
+    const bool tr = plan.trace && item < plan.trace_cap && threadIdx.x == 0;
+    if (tr) plan.trace[item * 8 + 0] = gtimer();
+    const uint32_t pk = plan.items[item];
+    const int s = (int)(pk >> 28);
+    const int seg = (int)((pk >> 16) & 0xfff);
+    const int d = (int)(pk & 0xffff);
+    const int dhi = d < f.nx - 1 ? d : f.nx - 1;
+    const int ii = plan.diag_lo[d] + seg * 32 + c;
+    const bool valid = ii <= dhi;
+    const int jj = d - ii;
+    const int dir = plan.dirs[s];
+    const bool i_up = dir == 0 || dir == 3, j_up = dir == 0 || dir == 1;  // kSweepDirs
+    const int i = valid ? (i_up ? ii : f.nx - 1 - ii) : 0;
+    const int j = valid ? (j_up ? jj : f.ny - 1 - jj) : 0;
+    // dependency wait (rule in sweep_persistent.cuh): partition 0 of each face
+    // group polls its face's neighbours, group 0 partition 1 the cell itself
+    if (valid && (q == 0 || (g == 0 && q == 1))) {
+      const int axis = g >> 1, side = g & 1;
+      bool ok = false;
+      long long polls = 0;
+      while (!ok) {
+        ok = true;
+        if (q == 1) {
+          if (ld_acquire(plan.ver + j * f.nx + i) < (unsigned)s) ok = false;
+        } else {
+#pragma unroll
+          for (int dist = 1; dist <= radius; ++dist) {
+            const int ni = axis == 0 ? (side ? i + dist : i - dist) : i;
+            const int nj = axis == 1 ? (side ? j + dist : j - dist) : j;
+            if (ni >= 0 && ni < f.nx && nj >= 0 && nj < f.ny) {
+              const bool before = axis == 0 ? (i_up ? ni < i : ni > i) : (j_up ? nj < j : nj > j);
+              if (ld_acquire(plan.ver + nj * f.nx + ni) < (unsigned)s + (before ? 1u : 0u)) ok = false;
+            }
+          }
+        }
+        if (!ok) {
+          if (*((volatile const int*)&err->code) != 0) break;
+          if (++polls > (1LL << 26)) {  // deadlock guard: fail loudly, never hang
+            tc::raise(err, E_ERROR, W_DEADLOCK, i, j, (double)s);
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tr) plan.trace[item * 8 + 1] = gtimer();
+    unsigned long long* st = tr ? plan.trace + item * 8 + 4 : nullptr;
+    int w = g < 2 ? face_split<M, ORDER, 0>(f, ctx, g, q, valid, i, j, L, U, F, st)
+                  : face_split<M, ORDER, 1>(f, ctx, g, q, valid, i, j, L, U, F, st);
+    if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, 0.0);
+    __syncthreads();
+    if (tr) plan.trace[item * 8 + 2] = gtimer();
+    w = W_NONE;
+    double bad = 0.0;
+    if (g == 0) {
+      w = update_split<M>(f, has_rhs ? &rhs : nullptr, ctx, q, valid, i, j, smem, &bad);
+      if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
+    }
+    __syncthreads();
+    if (tr) plan.trace[item * 8 + 3] = gtimer();
+    if (g == 0 && q == 0 && valid && w == W_NONE) st_release(plan.ver + j * f.nx + i, (unsigned)s + 1u);
+  }
+}
+
+}  // namespace sp
+}  // namespace momg_gpu

@@ -90,11 +90,16 @@ __global__ void __launch_bounds__(PWPB * 32) k_sweep_persistent(DevField f, DevF
       }
     }
     bool ready = false;
+    long long polls = 0;
     while (!ready) {
       bool mine = dn < 0 || ld_acquire(plan.ver + dn) >= need;
       ready = __all_sync(FULL, mine);
       if (!ready) {
         if (err_set(err)) return;
+        if (++polls > (1LL << 26)) {  // deadlock guard: fail loudly, never hang
+          if (lane == 0) raise_err(err, E_ERROR, W_DEADLOCK, i, j, (double)s);
+          return;
+        }
         __nanosleep(32);
       }
     }

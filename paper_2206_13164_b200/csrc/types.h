@@ -46,6 +46,7 @@ enum : int {
   W_FAS = 12,          // fas_correct: nonphysical after correction (SolverError)
   W_RESTRICT = 13,     // restrict_solution: nonphysical coarse state
   W_ES_UNSUPPORTED = 14,
+  W_DEADLOCK = 15,     // persistent sweep: dependency wait timed out (bug guard)
 };
 
 // Problem constants (SolveContext, single_level.hpp:27-34), by value per launch.

@@ -160,5 +160,133 @@ def main():
     print(out, len(text.splitlines()), "lines")
 
 
+# ---------------------------------------------------------------------------
+# Partitioned variants (split design): the same operations cut into P parts
+# of balanced cost, part q executed by warp q of a face group (lane = cell).
+# Vectors of the 32 cells of a segment interleave: element k of cell c at
+# v[k * 32 + c].  An axis pass is split by pencils, which are disjoint element
+# sets, so it runs in place; the half sums are split by the normal index p and
+# write a separate output vector.  One named barrier separates passes.
+
+def lpt(costs, P):
+    parts = [[] for _ in range(P)]
+    load = [0] * P
+    for key, c in sorted(costs.items(), key=lambda kv: -kv[1]):
+        q = load.index(min(load))
+        parts[q].append(key)
+        load[q] += c
+    return parts
+
+
+def emit_split(M, P):
+    idx = simplex(M)
+    pos = {a: k for k, a in enumerate(idx)}
+    N = len(idx)
+    L = []
+    w = L.append
+    w(f"template <>\nstruct Split<{M}, {P}> {{")
+    # passes: out-of-place src -> dst (every element written exactly once)
+    for d in range(3):
+        others = [o for o in range(3) if o != d]
+        pencils = {}
+        for a in idx:
+            pencils.setdefault((a[others[0]], a[others[1]]), []).append(a)
+        costs = {k: len(v) * (len(v) + 1) // 2 + 2 * len(v) for k, v in pencils.items()}
+        parts = lpt(costs, P)
+        for q in range(P):
+            w(f"  static __device__ __forceinline__ void pass{d}_{q}(double* __restrict__ v, const double* c) {{")
+            for key in parts[q]:
+                members = sorted(pencils[key], key=lambda a: a[d])
+                ks = [pos[a] for a in members]
+                if len(ks) < 2:
+                    continue
+                w("    {")
+                for j, k in enumerate(ks):
+                    w(f"      const double f{j} = v[{k} * 32];")
+                for j in range(len(ks) - 1, 0, -1):
+                    expr = f"f{j}"
+                    for n in range(1, j + 1):
+                        expr = f"fma(c[{n}], f{j - n}, {expr})"
+                    w(f"      v[{ks[j]} * 32] = {expr};")
+                w("    }")
+            w("  }")
+    # half sums split by the normal index p
+    for a in range(2):
+        tans = {}
+        for b in idx:
+            t = tuple(b[o] for o in range(3) if o != a)
+            tans.setdefault(t, []).append(b)
+        costs = {}
+        for p in range(M + 1):
+            costs[p] = sum(len(m) * 2 for m in tans.values() if len(m) > p)
+        parts = lpt(costs, P)
+        for single in (False, True):
+            for q in range(P):
+                name = f"half_one{a}_{q}" if single else f"half_sum{a}_{q}"
+                kt = f"const double (&Ku)[{M + 1}][{M + 1}]"
+                args = f"const double* __restrict__ Lv, {kt}, double* __restrict__ o" if single else \
+                    f"const double* __restrict__ Lv, const double* __restrict__ Rv, {kt}, const double (&Kl)[{M + 1}][{M + 1}], double* __restrict__ o"
+                w(f"  static __device__ __forceinline__ void {name}({args}) {{")
+                for t, members in tans.items():
+                    members = sorted(members, key=lambda b: b[a])
+                    ks = [pos[b] for b in members]
+                    ps = [p for p in parts[q] if p < len(ks)]
+                    if not ps:
+                        continue
+                    w("    {")
+                    for m, k in enumerate(ks):
+                        w(f"      const double l{m} = Lv[{k} * 32];")
+                        if not single:
+                            w(f"      const double r{m} = Rv[{k} * 32];")
+                    for p in ps:
+                        expr = None
+                        for m in range(len(ks)):
+                            expr = f"l{m} * Ku[{m}][{p}]" if expr is None else f"fma(l{m}, Ku[{m}][{p}], {expr})"
+                            if not single:
+                                expr = f"fma(r{m}, Kl[{m}][{p}], {expr})"
+                        w(f"      o[{ks[p]} * 32] = {expr};")
+                    w("    }")
+                w("  }")
+        w(f"  static constexpr int HALF_PMAX{a}[{P}] = {{" + ", ".join(str(max(p) if p else 0) for p in parts) + "};")
+    # full flux split by coefficient ranges
+    chunks = [list(range(N))[q::P] for q in range(P)]
+    for a in range(2):
+        for q in range(P):
+            w(f"  static __device__ __forceinline__ void full_flux{a}_{q}(const double* __restrict__ s, double* __restrict__ o, double un, double th) {{")
+            for k in chunks[q]:
+                b = idx[k]
+                expr = f"un * s[{k} * 32]"
+                if b[a] >= 1:
+                    dn = list(b); dn[a] -= 1
+                    expr = f"fma(th, s[{pos[tuple(dn)]} * 32], {expr})"
+                if sum(b) < M:
+                    up = list(b); up[a] += 1
+                    expr = f"fma({float(b[a] + 1)}, s[{pos[tuple(up)]} * 32], {expr})"
+                w(f"    o[{k} * 32] = {expr};")
+            w("  }")
+    # contiguous coefficient ranges for element-wise work
+    bounds = [round(q * N / P) for q in range(P + 1)]
+    w(f"  static constexpr int KLO[{P + 1}] = {{" + ", ".join(map(str, bounds)) + "};")
+    w("};")
+    return "\n".join(L)
+
+
+def main_split():
+    out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2206_13164_b200", "csrc", "gen", "split_gen.cuh")
+    body = ["// GENERATED by tools/gen_simplex.py -- do not edit.",
+            "// Partitioned straight-line multi-index operations (split design).",
+            "#pragma once", "", "namespace momg_gpu {", "", "template <int M, int P>", "struct Split;", ""]
+    for M in ORDERS:
+        body.append(emit_split(M, 4))
+        body.append("")
+    body.append("}  // namespace momg_gpu")
+    text = "\n".join(body) + "\n"
+    if not os.path.exists(out) or open(out).read() != text:
+        open(out, "w").write(text)
+    print(out, len(text.splitlines()), "lines")
+
+
 if __name__ == "__main__":
     main()
+    main_split()
