@@ -32,8 +32,9 @@ using tc::P4;
 template <int M>
 struct Layout {
   static constexpr int N = Gen<M>::N;
-  static constexpr int VEC = N * 32;  // doubles of one vector for the 32 cells
-  static constexpr size_t bytes = (size_t)G * 3 * VEC * sizeof(double) + 64;
+  static constexpr int VEC = N * SPV;  // doubles of one vector for the 32 cells (stride SPV)
+  // per group L, U, F; then SB (cell state) and RB (rhs) of the update
+  static constexpr size_t bytes = ((size_t)G * 3 + 2) * VEC * sizeof(double) + 64;
 };
 
 // Non-.aligned named barriers: lanes of one warp may reach them from
@@ -135,28 +136,28 @@ __device__ __forceinline__ void full_flux(int q, const double* s, double* o, dou
 }
 
 __device__ __forceinline__ double rep_u32(const double* v, const P4& p, int axis) {
-  return p.v[axis] + v[(1 + axis) * 32] / v[0];
+  return p.v[axis] + v[(1 + axis) * SPV] / v[0];
 }
 __device__ __forceinline__ double rep_theta32(const double* v, const P4& p) {
   const double rho = v[0];
   double trace = 0.0, fe2 = 0.0;
-  const double c1 = v[1 * 32], c2 = v[2 * 32], c3 = v[3 * 32];
-  trace += v[4 * 32];
+  const double c1 = v[1 * SPV], c2 = v[2 * SPV], c3 = v[3 * SPV];
+  trace += v[4 * SPV];
   fe2 += c1 * c1;
-  trace += v[7 * 32];
+  trace += v[7 * SPV];
   fe2 += c2 * c2;
-  trace += v[9 * 32];
+  trace += v[9 * SPV];
   fe2 += c3 * c3;
   return p.v[3] + (2.0 * trace - fe2 / rho) / (3.0 * rho);
 }
 __device__ __forceinline__ double grad_defect32(const double* v) {
   double defect = 0.0, trace = 0.0;
-  defect = tc::smax(defect, fabs(v[1 * 32]));
-  trace += v[4 * 32];
-  defect = tc::smax(defect, fabs(v[2 * 32]));
-  trace += v[7 * 32];
-  defect = tc::smax(defect, fabs(v[3 * 32]));
-  trace += v[9 * 32];
+  defect = tc::smax(defect, fabs(v[1 * SPV]));
+  trace += v[4 * SPV];
+  defect = tc::smax(defect, fabs(v[2 * SPV]));
+  trace += v[7 * SPV];
+  defect = tc::smax(defect, fabs(v[3 * SPV]));
+  trace += v[9 * SPV];
   defect = tc::smax(defect, fabs(trace));
   return defect / fabs(v[0]);
 }
@@ -180,7 +181,43 @@ struct Part {
 #pragma unroll
     for (int k = 0; k < CNT; ++k) r[k] = __ldcg(src + LO + k);
 #pragma unroll
-    for (int k = 0; k < CNT; ++k) dst[(LO + k) * 32] = r[k];
+    for (int k = 0; k < CNT; ++k) dst[(LO + k) * SPV] = r[k];
+  }
+  static __device__ __forceinline__ void load2(const double* __restrict__ s0, double* __restrict__ d0,
+                                               const double* __restrict__ s1, double* __restrict__ d1) {
+    double r0[CNT], r1[CNT];
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) {
+      r0[k] = __ldcg(s0 + LO + k);
+      r1[k] = __ldcg(s1 + LO + k);
+    }
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) {
+      d0[(LO + k) * SPV] = r0[k];
+      d1[(LO + k) * SPV] = r1[k];
+    }
+  }
+  static __device__ __forceinline__ void copy(const double* __restrict__ s, double* __restrict__ d) {
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) d[(LO + k) * SPV] = s[(LO + k) * SPV];
+  }
+  // second-order face states in place from raw L (lower) and U (upper):
+  //   L += offL (U - LL) rhL,  U += offU (UU - L) rhU  (spatial.cpp:34-80)
+  static __device__ __forceinline__ void recon2(double* L, double* U, const double* gLL, const double* gUU,
+                                                bool rl, bool ru, double offL, double rhL, double offU,
+                                                double rhU) {
+    double ll[CNT], uu[CNT];
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) {
+      ll[k] = rl ? __ldcg(gLL + LO + k) : 0.0;
+      uu[k] = ru ? __ldcg(gUU + LO + k) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < CNT; ++k) {
+      const double lk = L[(LO + k) * SPV], uk = U[(LO + k) * SPV];
+      if (rl) L[(LO + k) * SPV] = fma(offL, (uk - ll[k]) * rhL, lk);
+      if (ru) U[(LO + k) * SPV] = fma(offU, (uu[k] - lk) * rhU, uk);
+    }
   }
   // dst = c + off * (h - l) * rh  (second-order face state, spatial.cpp:64-80)
   static __device__ __forceinline__ void recon(const double* __restrict__ c, const double* __restrict__ l,
@@ -194,7 +231,7 @@ struct Part {
       rhh[k] = __ldcg(h + LO + k);
     }
 #pragma unroll
-    for (int k = 0; k < CNT; ++k) dst[(LO + k) * 32] = fma(off, (rhh[k] - rl[k]) * rh, rc[k]);
+    for (int k = 0; k < CNT; ++k) dst[(LO + k) * SPV] = fma(off, (rhh[k] - rl[k]) * rh, rc[k]);
   }
   // residual assembly (spatial.cpp:127-132, collision.hpp:120-127), update_delta
   // (single_level.cpp:64-70) and f + dt delta (apply_update :47)
@@ -217,23 +254,23 @@ struct Part {
             if (k == flat3((e == 0 ? 2 : 0) + (d == 0), (e == 1 ? 2 : 0) + (d == 1), (e == 2 ? 2 : 0) + (d == 2)))
               eq = shw * qv[d];
       }
-      const double sk = S[k * 32];
+      const double sk = S[k * SPV];
       double r = nu * (eq - sk);
-      r -= (Fxp[k * 32] - Fxm[k * 32]) * idx;
-      r -= (Fyp[k * 32] - Fym[k * 32]) * idy;
-      if (rhs) r -= RH[k * 32];
-      D[k * 32] = r;
-      V[k * 32] = fma(dt, r, sk);
+      r -= (Fxp[k * SPV] - Fxm[k * SPV]) * idx;
+      r -= (Fyp[k * SPV] - Fym[k * SPV]) * idy;
+      if (rhs) r -= RH[k * SPV];
+      D[k * SPV] = r;
+      V[k * SPV] = fma(dt, r, sk);
     }
   }
   static __device__ __forceinline__ void restep(const double* S, const double* D, double step, double* V) {
 #pragma unroll
-    for (int kk = 0; kk < CNT; ++kk) V[(LO + kk) * 32] = fma(step, D[(LO + kk) * 32], S[(LO + kk) * 32]);
+    for (int kk = 0; kk < CNT; ++kk) V[(LO + kk) * SPV] = fma(step, D[(LO + kk) * SPV], S[(LO + kk) * SPV]);
   }
   static __device__ __forceinline__ void store(const double* __restrict__ v, double* __restrict__ dst) {
     double r[CNT];
 #pragma unroll
-    for (int k = 0; k < CNT; ++k) r[k] = v[(LO + k) * 32];
+    for (int k = 0; k < CNT; ++k) r[k] = v[(LO + k) * SPV];
 #pragma unroll
     for (int k = 0; k < CNT; ++k) __stcg(dst + LO + k, r[k]);
   }
@@ -253,6 +290,25 @@ __device__ __forceinline__ void part_recon(int q, const double* c, const double*
 #undef SP_RC
 }
 template <int M>
+__device__ __forceinline__ void part_load2(int q, const double* s0, double* d0, const double* s1, double* d1) {
+#define SP_L2(Q) Part<M, Q>::load2(s0, d0, s1, d1)
+  SP_DISPATCH(q, SP_L2)
+#undef SP_L2
+}
+template <int M>
+__device__ __forceinline__ void part_copy(int q, const double* src, double* dst) {
+#define SP_CP(Q) Part<M, Q>::copy(src, dst)
+  SP_DISPATCH(q, SP_CP)
+#undef SP_CP
+}
+template <int M>
+__device__ __forceinline__ void part_recon2(int q, double* L, double* U, const double* gLL, const double* gUU,
+                                            bool rl, bool ru, double offL, double rhL, double offU, double rhU) {
+#define SP_R2(Q) Part<M, Q>::recon2(L, U, gLL, gUU, rl, ru, offL, rhL, offU, rhU)
+  SP_DISPATCH(q, SP_R2)
+#undef SP_R2
+}
+template <int M>
 __device__ __forceinline__ void part_store(int q, const double* v, double* dst) {
 #define SP_ST(Q) Part<M, Q>::store(v, dst)
   SP_DISPATCH(q, SP_ST)
@@ -263,15 +319,76 @@ __device__ __forceinline__ void part_store(int q, const double* v, double* dst) 
 // Face flux of face group g (AXIS = g/2, high = g%2) for cell (i, j) (lane),
 // partition q; result (cell basis) left in F.  `valid` false: barriers only.
 // Returns W_NONE or the failure kind (same in all partitions of the cell).
+// Phase 3 of one partition: kernels of its own half-flux columns only (so
+// the other partitions' columns are dead code), then its share of the
+// half / full flux.  Partition 0 also returns row 0 of the incoming-side
+// wall kernel for the wall closure.
+template <int M, int AXIS, int Q>
+__device__ __forceinline__ void flux_q(int branch, bool high, double un, double rs, const P4& fp, const double* L,
+                                       const double* U, double* F, double (&kin0)[M + 1]) {
+  if (branch == B_HALF || branch == B_WALL) {
+    double Ku[M + 1][M + 1], Kl[M + 1][M + 1];
+    tc::half_kernels<M>(un, rs, Ku, Kl);
+    if (branch == B_HALF) {
+      if constexpr (AXIS == 0) {
+        if constexpr (Q == 0) Split<M, P>::half_sum0_0(L, U, Ku, Kl, F);
+        else if constexpr (Q == 1) Split<M, P>::half_sum0_1(L, U, Ku, Kl, F);
+        else if constexpr (Q == 2) Split<M, P>::half_sum0_2(L, U, Ku, Kl, F);
+        else Split<M, P>::half_sum0_3(L, U, Ku, Kl, F);
+      } else {
+        if constexpr (Q == 0) Split<M, P>::half_sum1_0(L, U, Ku, Kl, F);
+        else if constexpr (Q == 1) Split<M, P>::half_sum1_1(L, U, Ku, Kl, F);
+        else if constexpr (Q == 2) Split<M, P>::half_sum1_2(L, U, Ku, Kl, F);
+        else Split<M, P>::half_sum1_3(L, U, Ku, Kl, F);
+      }
+    } else {
+      double Kw[M + 1][M + 1];
+#pragma unroll
+      for (int m = 0; m <= M; ++m)
+#pragma unroll
+        for (int p = 0; p <= M; ++p) Kw[m][p] = high ? Ku[m][p] : Kl[m][p];
+      if constexpr (AXIS == 0) {
+        if constexpr (Q == 0) Split<M, P>::half_one0_0(L, Kw, F);
+        else if constexpr (Q == 1) Split<M, P>::half_one0_1(L, Kw, F);
+        else if constexpr (Q == 2) Split<M, P>::half_one0_2(L, Kw, F);
+        else Split<M, P>::half_one0_3(L, Kw, F);
+      } else {
+        if constexpr (Q == 0) Split<M, P>::half_one1_0(L, Kw, F);
+        else if constexpr (Q == 1) Split<M, P>::half_one1_1(L, Kw, F);
+        else if constexpr (Q == 2) Split<M, P>::half_one1_2(L, Kw, F);
+        else Split<M, P>::half_one1_3(L, Kw, F);
+      }
+      if constexpr (Q == 0) {
+#pragma unroll
+        for (int p = 0; p <= M; ++p) kin0[p] = high ? Kl[0][p] : Ku[0][p];
+      }
+    }
+  } else if (branch == B_FULL_L || branch == B_FULL_R) {
+    const double* src = branch == B_FULL_L ? L : U;
+    if constexpr (AXIS == 0) {
+      if constexpr (Q == 0) Split<M, P>::full_flux0_0(src, F, fp.v[0], fp.v[3]);
+      else if constexpr (Q == 1) Split<M, P>::full_flux0_1(src, F, fp.v[0], fp.v[3]);
+      else if constexpr (Q == 2) Split<M, P>::full_flux0_2(src, F, fp.v[0], fp.v[3]);
+      else Split<M, P>::full_flux0_3(src, F, fp.v[0], fp.v[3]);
+    } else {
+      if constexpr (Q == 0) Split<M, P>::full_flux1_0(src, F, fp.v[1], fp.v[3]);
+      else if constexpr (Q == 1) Split<M, P>::full_flux1_1(src, F, fp.v[1], fp.v[3]);
+      else if constexpr (Q == 2) Split<M, P>::full_flux1_2(src, F, fp.v[1], fp.v[3]);
+      else Split<M, P>::full_flux1_3(src, F, fp.v[1], fp.v[3]);
+    }
+  }
+}
+
 __device__ __forceinline__ unsigned long long gtimer0() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 
-template <int M, int ORDER, int AXIS>
+template <int M, int ORDER, int AXIS, bool RHS>
 __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, int g, int q, bool valid,
-                                          int i, int j, double* L, double* U, double* F,
+                                          int i, int j, double* L, double* U, double* F, double* SB,
+                                          const DevField* rhsf, double* RB, P4* cp_out,
                                           unsigned long long* stamp = nullptr) {
   constexpr int NP = (Gen<M>::N + 3) & ~3;
   const bool high = g & 1;
@@ -286,46 +403,120 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
   P4 cp{}, lp{}, rp{}, fp{};
   const double* xc = AXIS == 0 ? f.xc : f.yc;
   const double* dd = AXIS == 0 ? f.dx : f.dy;
-  // ---- phase 0: face states (spatial.cpp:34-80) into L / U
+  // ---- phase 0: face states (spatial.cpp:34-80) into L / U.
+  // (a) each lane resolves its cell's face geometry, parameter records and
+  //     the second-order reconstruction decision (safe_face_state);
+  // (b) the group's warps then load the coefficient records cooperatively,
+  //     one record per warp instruction pair (coalesced 448-byte reads,
+  //     lane = coefficient), reconstruct in registers and transpose into the
+  //     interleaved vectors.  Warp q handles cells 8q..8q+7.
+  // Group 0 (x-low face: the upper cell is the cell itself) also stages the
+  // cell state (and the rhs) for the update in SB / RB.
+  bool at_wall = false, reconL = false, reconU = false;
+  size_t cl = cell, cu = cell;
+  double offL = 0.0, offU = 0.0, rhL = 1.0, rhU = 1.0;
   if (valid) {
+    at_wall = high ? pos == n - 1 : pos == 0;
+    const int pl = high ? pos : pos - 1, pu = pl + 1;
+    cl = (high || at_wall) ? cell : cell - stride;  // wall: the cell itself
+    cu = at_wall ? cell : cl + stride;
+    const bool rl = !at_wall && ORDER == 2 && pl > 0 && pl < n - 1;
+    const bool ru = !at_wall && ORDER == 2 && pu > 0 && pu < n - 1;
     cp = tc::ldp<true>(f.p + cell * 4);
-    const bool at_wall = high ? pos == n - 1 : pos == 0;
-    if (at_wall) {
-      branch = B_WALL;
-      part_load<M>(q, f.c + cell * NP, L);
-    } else {
-      branch = B_HALF;
-      const int pl = high ? pos : pos - 1, pu = pl + 1;
-      const size_t cl = high ? cell : cell - stride, cu = cl + stride;
-      // lower state on its high side, upper state on its low side
-      for (int side = 0; side < 2; ++side) {
-        const int pc = side == 0 ? pl : pu;
-        const size_t cc = side == 0 ? cl : cu;
-        double* dst = side == 0 ? L : U;
-        P4 pr = tc::ldp<true>(f.p + cc * 4);
-        bool recon = false;
-        size_t lo = cc, hi = cc;
-        double off = 0.0, h = 1.0;
-        if (ORDER == 2 && pc > 0 && pc < n - 1) {
-          lo = cc - stride;
-          hi = cc + stride;
-          h = xc[pc + 1] - xc[pc - 1];
-          off = (side == 0 ? 0.5 : -0.5) * dd[pc];
-          const P4 pl4 = tc::ldp<true>(f.p + lo * 4), ph4 = tc::ldp<true>(f.p + hi * 4);
-          P4 w;
+    P4 pL = cp, pU = cp, pLL = cp, pUU = cp;
+    if (!at_wall) {
+      pL = tc::ldp<true>(f.p + cl * 4);
+      pU = tc::ldp<true>(f.p + cu * 4);
+    }
+    if (rl) pLL = tc::ldp<true>(f.p + (cl - stride) * 4);
+    if (ru) pUU = tc::ldp<true>(f.p + (cu + stride) * 4);
+    const double hl = rl ? xc[pl + 1] - xc[pl - 1] : 1.0;
+    const double hu = ru ? xc[pu + 1] - xc[pu - 1] : 1.0;
+    offL = 0.5 * dd[pl < 0 ? 0 : pl];
+    offU = -0.5 * dd[pu < n ? pu : n - 1];
+    rhL = 1.0 / hl;
+    rhU = 1.0 / hu;
+    branch = at_wall ? B_WALL : B_HALF;
+    lp = pL;
+    rp = pU;
+    if (rl) {
+      P4 w;
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) w.v[qq] = pr.v[qq] + off * ((ph4.v[qq] - pl4.v[qq]) / h);
-          if (w.v[3] > 0.0) {
-            recon = true;
-            pr = w;
+      for (int qq = 0; qq < 4; ++qq) w.v[qq] = pL.v[qq] + offL * ((pU.v[qq] - pLL.v[qq]) / hl);
+      if (w.v[3] > 0.0) {
+        reconL = true;
+        lp = w;
+      }
+    }
+    if (ru) {
+      P4 w;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) w.v[qq] = pU.v[qq] + offU * ((pUU.v[qq] - pL.v[qq]) / hu);
+      if (w.v[3] > 0.0) {
+        reconU = true;
+        rp = w;
+      }
+    }
+  }
+  {
+    constexpr int N = Gen<M>::N;
+    const int lane = threadIdx.x & 31;
+    double* Lb = L - lane;  // group vectors (cell 0 base)
+    double* Ub = U - lane;
+    double* Sb = SB ? SB - lane : nullptr;
+    double* Rb = RB ? RB - lane : nullptr;
+    const int flags = (valid ? 1 : 0) | (at_wall ? 2 : 0) | (reconL ? 4 : 0) | (reconU ? 8 : 0);
+    constexpr int H = (N + 31) / 32;
+    constexpr int B = 4;  // cells per batch: all their loads in flight at once
+#pragma unroll
+    for (int t0 = 0; t0 < 8; t0 += B) {
+      double Lr[B][H], Ur[B][H], Sr[B][H], Rr[B][H];
+      int fls[B];
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        const int cc = 8 * q + t0 + t;
+        const int fl = __shfl_sync(0xffffffffu, flags, cc);
+        fls[t] = fl;
+        const long long bl = __shfl_sync(0xffffffffu, (long long)cl, cc);
+        const long long bu = __shfl_sync(0xffffffffu, (long long)cu, cc);
+        const long long bs = __shfl_sync(0xffffffffu, (long long)cell, cc);
+        const double oL = __shfl_sync(0xffffffffu, offL, cc), oU = __shfl_sync(0xffffffffu, offU, cc);
+        const double hL = __shfl_sync(0xffffffffu, rhL, cc), hU = __shfl_sync(0xffffffffu, rhU, cc);
+        const bool ok = fl & 1, wall = fl & 2, rL = fl & 4, rU = fl & 8;
+        const double* gl = f.c + (size_t)bl * NP;
+        const double* gu = f.c + (size_t)bu * NP;
+        const double* gll = f.c + (size_t)(bl - (rL ? (long long)stride : 0)) * NP;
+        const double* guu = f.c + (size_t)(bu + (rU ? (long long)stride : 0)) * NP;
+        const double* gr = RHS ? rhsf->c + (size_t)bs * NP : nullptr;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int k = lane + 32 * h;
+          const bool in = ok && k < N;
+          const double lk = in ? __ldcg(gl + k) : 0.0;
+          const double uk = (in && !wall) ? __ldcg(gu + k) : 0.0;
+          const double llk = (in && rL) ? __ldcg(gll + k) : 0.0;
+          const double uuk = (in && rU) ? __ldcg(guu + k) : 0.0;
+          Rr[t][h] = (RHS && g == 0 && in) ? __ldcg(gr + k) : 0.0;
+          Lr[t][h] = rL ? fma(oL, (uk - llk) * hL, lk) : lk;
+          Ur[t][h] = rU ? fma(oU, (uuk - lk) * hU, uk) : uk;
+          Sr[t][h] = wall ? lk : uk;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        const int cc = 8 * q + t0 + t;
+        if (!(fls[t] & 1)) continue;
+        const bool wall = fls[t] & 2;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+          const int k = lane + 32 * h;
+          if (k < N) {
+            Lb[k * SPV + cc] = Lr[t][h];
+            if (!wall) Ub[k * SPV + cc] = Ur[t][h];
+            if (g == 0) Sb[k * SPV + cc] = Sr[t][h];
+            if (RHS && g == 0) Rb[k * SPV + cc] = Rr[t][h];
           }
         }
-        const double* sc = f.c + cc * NP;
-        if (recon)
-          part_recon<M>(q, sc, f.c + lo * NP, f.c + hi * NP, off, 1.0 / h, dst);
-        else
-          part_load<M>(q, sc, dst);
-        if (side == 0) lp = pr; else rp = pr;
       }
     }
   }
@@ -369,22 +560,19 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
                 U, rp, fp, branch == B_HALF || branch == B_FULL_R);
   }
   if (stamp) stamp[1] = gtimer0();
-  // ---- phase 3: flux in the face basis into F
-  double Ku[M + 1][M + 1], Kl[M + 1][M + 1];
-  if (branch == B_HALF || branch == B_WALL) {
-    tc::half_kernels<M>(branch == B_WALL ? 0.0 : fp.v[AXIS], rs, Ku, Kl);
-    if (branch == B_HALF) half_sum<M, AXIS>(q, L, U, Ku, Kl, F);
-    else half_one<M, AXIS>(q, L, high ? Ku : Kl, F);
-  } else if (branch == B_FULL_L) {
-    full_flux<M, AXIS>(q, L, F, fp.v[AXIS], fp.v[3]);
-  } else if (branch == B_FULL_R) {
-    full_flux<M, AXIS>(q, U, F, fp.v[AXIS], fp.v[3]);
+  // ---- phase 3: flux in the face basis into F (per-partition K columns)
+  double kin0[M + 1];
+  {
+    const double un = branch == B_WALL ? 0.0 : fp.v[AXIS];
+#define SP_FQ(Q) flux_q<M, AXIS, Q>(branch, high, un, rs, fp, L, U, F, kin0)
+    SP_DISPATCH(q, SP_FQ)
+#undef SP_FQ
   }
   gbar(g);
   if (stamp) stamp[2] = gtimer0();
   // wall closure: density of the incoming wall Maxwellian (flux.cpp:119-129)
   if (branch == B_WALL && q == 0) {
-    const double in0 = high ? Kl[0][0] : Ku[0][0];
+    const double in0 = kin0[0];
     const double wall_rho = in0 == 0.0 ? 0.0 : -F[0] / in0;
     if (in0 == 0.0) {
       fail = W_WALL_DEGEN;
@@ -394,7 +582,7 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
 #pragma unroll
       for (int p = 1; p <= M; ++p) {
         const int k = AXIS == 0 ? flat3(p, 0, 0) : flat3(0, p, 0);
-        F[k * 32] = fma(wall_rho, high ? Kl[0][p] : Ku[0][p], F[k * 32]);
+        F[k * SPV] = fma(wall_rho, kin0[p], F[k * SPV]);
       }
       F[0] = 0.0;
     }
@@ -403,6 +591,7 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
   // ---- phase 4: flux back into the cell basis (in F)
   const P4 from = branch == B_WALL ? wb : fp;
   project2<M>(g, q, F, from, cp, branch != B_NONE, U, cp, cp, false);
+  *cp_out = cp;
   return fail;
 }
 
@@ -412,11 +601,12 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
 // grad_normalize with the dt/2 retry (apply_update :44-62); face group 0.
 template <int M>
 __device__ __forceinline__ int update_split(const DevField& f, const DevField* rhs, const DevCtx& ctx,
-                                            int q, bool valid, int i, int j, double* base, double* bad) {
+                                            int q, bool valid, int i, int j, double* base, double* bad,
+                                            P4 cp) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, VEC = Layout<M>::VEC;
   const int c = threadIdx.x & 31;
-  double* S = base + 0 * VEC + c;       // L_0
-  double* RH = base + 1 * VEC + c;      // U_0
+  double* S = base + 12 * VEC + c;      // SB (staged in the face phase)
+  double* RH = base + 13 * VEC + c;     // RB
   double* V = base + 3 * VEC + c;       // L_1
   double* D = base + 4 * VEC + c;       // U_1
   const double* Fxm = base + 2 * VEC + c;
@@ -426,16 +616,8 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
   int klo, khi;
   krange<M>(q, &klo, &khi);
   const size_t cell = (size_t)j * f.nx + i;
-  P4 cp{}, rp{};
-  if (valid) {
-    cp = tc::ldp<true>(f.p + cell * 4);
-    part_load<M>(q, f.c + cell * NP, S);
-    if (rhs) {
-      rp = tc::ldp<true>(rhs->p + cell * 4);
-      part_load<M>(q, rhs->c + cell * NP, RH);
-    }
-  }
-  gbar(0);
+  P4 rp{};
+  if (valid && rhs) rp = tc::ldp<true>(rhs->p + cell * 4);
   int fail = W_NONE;
   double dt = 0.0, nu = 0.0, qv[3] = {0.0, 0.0, 0.0};
   if (valid) {
@@ -450,9 +632,9 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
       else {
         nu = ctx.nu_coef * rho * pow(cp.v[3], ctx.nu_exp);
         if (ctx.collision == 2) {
-          qv[0] = 2.0 * S[flat3(3, 0, 0) * 32] + S[flat3(3, 0, 0) * 32] + S[flat3(1, 2, 0) * 32] + S[flat3(1, 0, 2) * 32];
-          qv[1] = 2.0 * S[flat3(0, 3, 0) * 32] + S[flat3(2, 1, 0) * 32] + S[flat3(0, 3, 0) * 32] + S[flat3(0, 1, 2) * 32];
-          qv[2] = 2.0 * S[flat3(0, 0, 3) * 32] + S[flat3(2, 0, 1) * 32] + S[flat3(0, 2, 1) * 32] + S[flat3(0, 0, 3) * 32];
+          qv[0] = 2.0 * S[flat3(3, 0, 0) * SPV] + S[flat3(3, 0, 0) * SPV] + S[flat3(1, 2, 0) * SPV] + S[flat3(1, 0, 2) * SPV];
+          qv[1] = 2.0 * S[flat3(0, 3, 0) * SPV] + S[flat3(2, 1, 0) * SPV] + S[flat3(0, 3, 0) * SPV] + S[flat3(0, 1, 2) * SPV];
+          qv[2] = 2.0 * S[flat3(0, 0, 3) * SPV] + S[flat3(2, 0, 1) * SPV] + S[flat3(0, 2, 1) * SPV] + S[flat3(0, 0, 3) * SPV];
         }
       }
     }
@@ -536,11 +718,27 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
     }
     if (!gbar_or(0, !done)) break;
   }
-  if (valid && fail == W_NONE && good) {
-    part_store<M>(q, V, f.c + cell * NP);
-    if (q == 0) {
+  // coalesced write-back: warp q stores cells 8q..8q+7, lane = coefficient
+  {
+    const int lane = threadIdx.x & 31;
+    const bool ok = valid && fail == W_NONE && good;
+    if (ok && q == 0) {
       __stcg(reinterpret_cast<double2*>(f.p + cell * 4), make_double2(prm.v[0], prm.v[1]));
       __stcg(reinterpret_cast<double2*>(f.p + cell * 4) + 1, make_double2(prm.v[2], prm.v[3]));
+    }
+    const double* Vb = V - lane;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int cc = 8 * q + t;
+      const int okc = __shfl_sync(0xffffffffu, ok ? 1 : 0, cc);
+      const long long bc = __shfl_sync(0xffffffffu, (long long)cell, cc);
+      if (!okc) continue;
+      double* dst = f.c + (size_t)bc * NP;
+#pragma unroll
+      for (int h = 0; h < (N + 31) / 32; ++h) {
+        const int k = lane + 32 * h;
+        if (k < N) __stcg(dst + k, Vb[k * SPV + cc]);
+      }
     }
     __threadfence();
   }
@@ -630,15 +828,23 @@ __global__ void __launch_bounds__(THREADS, 1) k4_sweep(DevField f, DevField rhs,
     __syncthreads();
     if (tr) plan.trace[item * 8 + 1] = gtimer();
     unsigned long long* st = tr ? plan.trace + item * 8 + 4 : nullptr;
-    int w = g < 2 ? face_split<M, ORDER, 0>(f, ctx, g, q, valid, i, j, L, U, F, st)
-                  : face_split<M, ORDER, 1>(f, ctx, g, q, valid, i, j, L, U, F, st);
+    double* SB = smem + 12 * VEC + c;
+    double* RB = smem + 13 * VEC + c;
+    P4 cpv{};
+    int w;
+    if (has_rhs)
+      w = g < 2 ? face_split<M, ORDER, 0, true>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st)
+                : face_split<M, ORDER, 1, true>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st);
+    else
+      w = g < 2 ? face_split<M, ORDER, 0, false>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st)
+                : face_split<M, ORDER, 1, false>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st);
     if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, 0.0);
     __syncthreads();
     if (tr) plan.trace[item * 8 + 2] = gtimer();
     w = W_NONE;
     double bad = 0.0;
     if (g == 0) {
-      w = update_split<M>(f, has_rhs ? &rhs : nullptr, ctx, q, valid, i, j, smem, &bad);
+      w = update_split<M>(f, has_rhs ? &rhs : nullptr, ctx, q, valid, i, j, smem, &bad, cpv);
       if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
     }
     __syncthreads();

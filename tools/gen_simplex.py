@@ -202,12 +202,12 @@ def emit_split(M, P):
                     continue
                 w("    {")
                 for j, k in enumerate(ks):
-                    w(f"      const double f{j} = v[{k} * 32];")
+                    w(f"      const double f{j} = v[{k} * SPV];")
                 for j in range(len(ks) - 1, 0, -1):
                     expr = f"f{j}"
                     for n in range(1, j + 1):
                         expr = f"fma(c[{n}], f{j - n}, {expr})"
-                    w(f"      v[{ks[j]} * 32] = {expr};")
+                    w(f"      v[{ks[j]} * SPV] = {expr};")
                 w("    }")
             w("  }")
     # half sums split by the normal index p
@@ -235,16 +235,16 @@ def emit_split(M, P):
                         continue
                     w("    {")
                     for m, k in enumerate(ks):
-                        w(f"      const double l{m} = Lv[{k} * 32];")
+                        w(f"      const double l{m} = Lv[{k} * SPV];")
                         if not single:
-                            w(f"      const double r{m} = Rv[{k} * 32];")
+                            w(f"      const double r{m} = Rv[{k} * SPV];")
                     for p in ps:
                         expr = None
                         for m in range(len(ks)):
                             expr = f"l{m} * Ku[{m}][{p}]" if expr is None else f"fma(l{m}, Ku[{m}][{p}], {expr})"
                             if not single:
                                 expr = f"fma(r{m}, Kl[{m}][{p}], {expr})"
-                        w(f"      o[{ks[p]} * 32] = {expr};")
+                        w(f"      o[{ks[p]} * SPV] = {expr};")
                     w("    }")
                 w("  }")
         w(f"  static constexpr int HALF_PMAX{a}[{P}] = {{" + ", ".join(str(max(p) if p else 0) for p in parts) + "};")
@@ -255,14 +255,14 @@ def emit_split(M, P):
             w(f"  static __device__ __forceinline__ void full_flux{a}_{q}(const double* __restrict__ s, double* __restrict__ o, double un, double th) {{")
             for k in chunks[q]:
                 b = idx[k]
-                expr = f"un * s[{k} * 32]"
+                expr = f"un * s[{k} * SPV]"
                 if b[a] >= 1:
                     dn = list(b); dn[a] -= 1
-                    expr = f"fma(th, s[{pos[tuple(dn)]} * 32], {expr})"
+                    expr = f"fma(th, s[{pos[tuple(dn)]} * SPV], {expr})"
                 if sum(b) < M:
                     up = list(b); up[a] += 1
-                    expr = f"fma({float(b[a] + 1)}, s[{pos[tuple(up)]} * 32], {expr})"
-                w(f"    o[{k} * 32] = {expr};")
+                    expr = f"fma({float(b[a] + 1)}, s[{pos[tuple(up)]} * SPV], {expr})"
+                w(f"    o[{k} * SPV] = {expr};")
             w("  }")
     # contiguous coefficient ranges for element-wise work
     bounds = [round(q * N / P) for q in range(P + 1)]
@@ -276,7 +276,10 @@ def main_split():
                        "paper_2206_13164_b200", "csrc", "gen", "split_gen.cuh")
     body = ["// GENERATED by tools/gen_simplex.py -- do not edit.",
             "// Partitioned straight-line multi-index operations (split design).",
-            "#pragma once", "", "namespace momg_gpu {", "", "template <int M, int P>", "struct Split;", ""]
+            "// SPV: element stride of the interleaved per-cell vectors (odd, so",
+            "// a warp writing one cell's elements is bank-conflict free too).",
+            "#pragma once", "", "#ifndef SPV", "#define SPV 33", "#endif", "",
+            "namespace momg_gpu {", "", "template <int M, int P>", "struct Split;", ""]
     for M in ORDERS:
         body.append(emit_split(M, 4))
         body.append("")
