@@ -224,3 +224,53 @@ def test_nonconvergence_carries_report():
     with pytest.raises(momg.NonConvergence) as ei:
         momg.solve_steady(f, ctx, momg.SolverOptions(momg.SolverKind.fs, 1e-8, 3))
     assert ei.value.report.iterations == 3 and len(ei.value.report.history) == 3
+
+
+def _golden(name):
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name))
+
+
+def _macro_rel(got, want):
+    # relative to each quantity's own scale (rho, u, theta, q, sigma columns)
+    scale = np.maximum(np.max(np.abs(want), axis=0), 1e-12)
+    return float(np.max(np.abs(got - want) / scale))
+
+
+def test_c1_against_reference_golden():
+    """BASELINE configs[0] (C1): 32^2, M=3, first order, BGK Kn 0.1, FS to 1e-8.
+    Golden = the reference's own run (302 iterations)."""
+    z = _golden("c1.npz")
+    M = 3
+    g = Grid.uniform(32, 32)
+    octx = cavity_ctx(M, 1, BGK, kn=0.1, lid=0.1)
+    octx.c_bound = octx.cfl_c_bound = float(z["c_bound"])
+    c, p = uniform_field(g, M)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    rep = momg.solve_steady(f, mctx(octx), momg.SolverOptions(momg.SolverKind.fs, 1e-8))
+    assert rep.converged and abs(rep.iterations - int(z["iterations"])) <= 1
+    gc, gp = f.download()
+    assert _macro_rel(macro(gc, gp), macro(z["coeffs"], z["params"])) <= 1e-8
+
+
+def test_c2_against_reference_golden():
+    """BASELINE configs[1] (C2): 128^2, M=5, second order, BGK Kn 0.1, NMG over
+    4 levels (V(2,2), s3=4) to 1e-8.  Golden = the CPU oracle run (99 NMG
+    iterations, 1065 s single-threaded), pinned bitwise to the reference."""
+    z = _golden("c2.npz")
+    M = 5
+    g = Grid.uniform(128, 128)
+    octx = cavity_ctx(M, 2, BGK, kn=0.1, lid=0.1)
+    octx.c_bound = octx.cfl_c_bound = float(z["c_bound"])
+    c, p = uniform_field(g, M)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    rep = momg.solve_steady(f, mctx(octx), momg.SolverOptions(momg.SolverKind.nmg, 1e-8, 0, 4))
+    assert rep.converged and abs(rep.iterations - int(z["iterations"])) <= 1
+    gc, gp = f.download()
+    q = np.stack([3 * gc[:, 10] + gc[:, 13] + gc[:, 15], 3 * gc[:, 16] + gc[:, 11] + gc[:, 18]], axis=1)
+    mg = np.concatenate([gc[:, :1], gp, q, 2 * gc[:, 4:5], gc[:, 5:6], 2 * gc[:, 7:8]], axis=1)
+    want = z["macro"]
+    # u_z is identically zero in the cavity: compare it absolutely
+    cols = [k for k in range(want.shape[1]) if k != 3]
+    assert _macro_rel(mg[:, cols], want[:, cols]) <= 1e-8
+    assert np.max(np.abs(mg[:, 3])) <= 1e-12
