@@ -259,6 +259,16 @@ class Oracle:
             return c, p, ev.value
         return c, p, ev.value, rc, err.msg.decode(errors="replace")
 
+    def sweep_cells(self, ctx: Ctx, g: Grid, coeffs, params, cells, rhs=None):
+        """sweep_cell for each (i, j) in order, IN PLACE on coeffs/params
+        (C-contiguous float64 arrays).  Port only (test infrastructure)."""
+        cl = np.ascontiguousarray(np.asarray(cells, dtype=np.int32).reshape(-1, 2))
+        err = MoErr(); cc = ctx.c(); gg = g.c()
+        rc_, rp_ = (None, None) if rhs is None else (rhs[0], rhs[1])
+        self._check(self.lib.mo_sweep_cells(C.byref(cc), C.byref(gg), _ptr(coeffs), _ptr(params),
+                                            _ptr(rc_), _ptr(rp_), cl.ctypes.data_as(_ip), len(cl),
+                                            C.byref(err)), err)
+
     def total_mass(self, g: Grid, M, coeffs):
         gg = g.c()
         return self.lib.mo_total_mass(C.byref(gg), M, _ptr(_arr(coeffs)))

@@ -789,6 +789,22 @@ int mo_fast_sweep(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* p
   return fast_sweep(ctx, &f, rhs_coeffs, rhs_params, sweep_order, evals, err);
 }
 
+/* sweep_cell (single_level.cpp:103-111) applied to an explicit list of cells
+ * in the given order: the building block of the distributed (row-strip)
+ * sweep tests, where each rank updates its own cells of a global-size array
+ * whose rows outside its strip + halo are stale. */
+int mo_sweep_cells(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
+                   const double* rhs_coeffs, const double* rhs_params, const int* cells, int n,
+                   mo_err* err) {
+  clear(err);
+  fieldv f = {g, get_set(ctx->M), coeffs, params};
+  for (int q = 0; q < n; ++q) {
+    const int i = cells[2 * q], j = cells[2 * q + 1];
+    TRY(sweep_cell(ctx, &f, i, j, rhs_coeffs, rhs_params, err));
+  }
+  return MO_OK;
+}
+
 /* global_dt, single_level.cpp:31-38 */
 static int global_dt(const mo_ctx* ctx, const fieldv* f, double* dt_out, mo_err* err) {
   double dt = INFINITY;

@@ -132,6 +132,9 @@ int mo_solve_steady(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double*
 int mo_nmg_cycle(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
                  int levels, int s1, int s2, int s3, int gamma, long long* work,
                  mo_err* err);
+int mo_sweep_cells(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
+                   const double* rhs_coeffs, const double* rhs_params, const int* cells, int n,
+                   mo_err* err);
 int mo_euler_step(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
                   mo_err* err);
 
