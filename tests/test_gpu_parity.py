@@ -274,3 +274,20 @@ def test_c2_against_reference_golden():
     cols = [k for k in range(want.shape[1]) if k != 3]
     assert _macro_rel(mg[:, cols], want[:, cols]) <= 1e-8
     assert np.max(np.abs(mg[:, 3])) <= 1e-12
+
+
+def test_reference_program_through_bridge():
+    """The reference's own C++ (its Grid2D/SolveContext/solve_steady), switched
+    to the B200 by integration/momg_gpu_bridge.hpp: C1 on CPU (reference) and
+    GPU agree (iterations +-1, macro 1e-8).  Binary built here by
+    `make -C oracle bridge` (needs the reference sources) and shipped."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "bridge_demo")
+    if not os.path.exists(exe):
+        pytest.skip("bridge_demo not built (needs /root/reference at build time)")
+    out = subprocess.run([exe, "32"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    import json
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["cpu_iterations"] == 302 and abs(d["gpu_iterations"] - 302) <= 1
