@@ -404,117 +404,133 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
   const double* xc = AXIS == 0 ? f.xc : f.yc;
   const double* dd = AXIS == 0 ? f.dx : f.dy;
   // ---- phase 0: face states (spatial.cpp:34-80) into L / U.
-  // (a) each lane resolves its cell's face geometry, parameter records and
-  //     the second-order reconstruction decision (safe_face_state);
-  // (b) the group's warps then load the coefficient records cooperatively,
-  //     one record per warp instruction pair (coalesced 448-byte reads,
-  //     lane = coefficient), reconstruct in registers and transpose into the
-  //     interleaved vectors.  Warp q handles cells 8q..8q+7.
-  // Group 0 (x-low face: the upper cell is the cell itself) also stages the
-  // cell state (and the rhs) for the update in SB / RB.
-  bool at_wall = false, reconL = false, reconU = false;
-  size_t cl = cell, cu = cell;
-  double offL = 0.0, offU = 0.0, rhL = 1.0, rhU = 1.0;
-  if (valid) {
-    at_wall = high ? pos == n - 1 : pos == 0;
-    const int pl = high ? pos : pos - 1, pu = pl + 1;
-    cl = (high || at_wall) ? cell : cell - stride;  // wall: the cell itself
-    cu = at_wall ? cell : cl + stride;
-    const bool rl = !at_wall && ORDER == 2 && pl > 0 && pl < n - 1;
-    const bool ru = !at_wall && ORDER == 2 && pu > 0 && pu < n - 1;
-    cp = tc::ldp<true>(f.p + cell * 4);
-    P4 pL = cp, pU = cp, pLL = cp, pUU = cp;
-    if (!at_wall) {
-      pL = tc::ldp<true>(f.p + cl * 4);
-      pU = tc::ldp<true>(f.p + cu * 4);
-    }
-    if (rl) pLL = tc::ldp<true>(f.p + (cl - stride) * 4);
-    if (ru) pUU = tc::ldp<true>(f.p + (cu + stride) * 4);
-    const double hl = rl ? xc[pl + 1] - xc[pl - 1] : 1.0;
-    const double hu = ru ? xc[pu + 1] - xc[pu - 1] : 1.0;
-    offL = 0.5 * dd[pl < 0 ? 0 : pl];
-    offU = -0.5 * dd[pu < n ? pu : n - 1];
-    rhL = 1.0 / hl;
-    rhU = 1.0 / hu;
-    branch = at_wall ? B_WALL : B_HALF;
-    lp = pL;
-    rp = pU;
-    if (rl) {
-      P4 w;
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) w.v[qq] = pL.v[qq] + offL * ((pU.v[qq] - pLL.v[qq]) / hl);
-      if (w.v[3] > 0.0) {
-        reconL = true;
-        lp = w;
-      }
-    }
-    if (ru) {
-      P4 w;
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) w.v[qq] = pU.v[qq] + offU * ((pUU.v[qq] - pL.v[qq]) / hu);
-      if (w.v[3] > 0.0) {
-        reconU = true;
-        rp = w;
-      }
-    }
-  }
+  // Each lane (= cell) resolves its face geometry and publishes a small
+  // descriptor in warp-private scratch (this group's F vector, unused until
+  // phase 3).  The warp then loads the coefficient records of cells
+  // 8q..8q+7 cooperatively (lane = coefficient, coalesced 448-byte reads),
+  // all of a batch in flight at once, while each lane fetches its cell's
+  // parameter records and decides the second-order reconstruction
+  // (safe_face_state); a second descriptor pass applies the decisions and
+  // transposes into the interleaved vectors.  Group 0 (x-low face: the upper
+  // cell is the cell itself) also stages the cell state (and rhs) in SB / RB.
   {
     constexpr int N = Gen<M>::N;
+    constexpr int H = (N + 31) / 32;
+    constexpr int B = ORDER == 2 ? 2 : 4;  // cells per load batch
     const int lane = threadIdx.x & 31;
-    double* Lb = L - lane;  // group vectors (cell 0 base)
+    double* Fbase = F - lane;
+    // 128 doubles per warp: fits the smallest F vector (M=3: 20 x 33)
+    static_assert(4 * 128 <= N * SPV, "phase-0 scratch exceeds the F vector");
+    double* DaL = Fbase + q * 128;
+    double* DaU = DaL + 32;
+    int* Dcl = reinterpret_cast<int*>(DaL + 64);
+    int* Dcu = Dcl + 32;
+    int* Dfl = Dcl + 64;
+    int* Ddec = Dcl + 96;
+    bool at_wall = false, rl = false, ru = false;
+    size_t cl = cell, cu = cell;
+    int pl = pos, pu = pos;
+    if (valid) {
+      at_wall = high ? pos == n - 1 : pos == 0;
+      pl = high ? pos : pos - 1;
+      pu = pl + 1;
+      cl = (high || at_wall) ? cell : cell - stride;  // wall: the cell itself
+      cu = at_wall ? cell : cl + stride;
+      rl = !at_wall && ORDER == 2 && pl > 0 && pl < n - 1;
+      ru = !at_wall && ORDER == 2 && pu > 0 && pu < n - 1;
+    }
+    Dcl[lane] = (int)cl;
+    Dcu[lane] = (int)cu;
+    Dfl[lane] = (valid ? 1 : 0) | (at_wall ? 2 : 0) | (rl ? 4 : 0) | (ru ? 8 : 0);
+    __syncwarp();
+    double* Lb = L - lane;
     double* Ub = U - lane;
     double* Sb = SB ? SB - lane : nullptr;
     double* Rb = RB ? RB - lane : nullptr;
-    const int flags = (valid ? 1 : 0) | (at_wall ? 2 : 0) | (reconL ? 4 : 0) | (reconU ? 8 : 0);
-    constexpr int H = (N + 31) / 32;
-    constexpr int B = 4;  // cells per batch: all their loads in flight at once
 #pragma unroll
     for (int t0 = 0; t0 < 8; t0 += B) {
-      double Lr[B][H], Ur[B][H], Sr[B][H], Rr[B][H];
-      int fls[B];
+      // (1) issue every coefficient load of the batch
+      double lk[B][H], uk[B][H], llk[B][H], uuk[B][H], rk[B][H];
 #pragma unroll
       for (int t = 0; t < B; ++t) {
         const int cc = 8 * q + t0 + t;
-        const int fl = __shfl_sync(0xffffffffu, flags, cc);
-        fls[t] = fl;
-        const long long bl = __shfl_sync(0xffffffffu, (long long)cl, cc);
-        const long long bu = __shfl_sync(0xffffffffu, (long long)cu, cc);
-        const long long bs = __shfl_sync(0xffffffffu, (long long)cell, cc);
-        const double oL = __shfl_sync(0xffffffffu, offL, cc), oU = __shfl_sync(0xffffffffu, offU, cc);
-        const double hL = __shfl_sync(0xffffffffu, rhL, cc), hU = __shfl_sync(0xffffffffu, rhU, cc);
-        const bool ok = fl & 1, wall = fl & 2, rL = fl & 4, rU = fl & 8;
-        const double* gl = f.c + (size_t)bl * NP;
-        const double* gu = f.c + (size_t)bu * NP;
-        const double* gll = f.c + (size_t)(bl - (rL ? (long long)stride : 0)) * NP;
-        const double* guu = f.c + (size_t)(bu + (rU ? (long long)stride : 0)) * NP;
-        const double* gr = RHS ? rhsf->c + (size_t)bs * NP : nullptr;
+        const int fl = Dfl[cc];
+        const bool ok = fl & 1, wall = fl & 2, el = fl & 4, eu = fl & 8;
+        const double* gl = f.c + (size_t)Dcl[cc] * NP;
+        const double* gu = f.c + (size_t)Dcu[cc] * NP;
 #pragma unroll
         for (int h = 0; h < H; ++h) {
           const int k = lane + 32 * h;
           const bool in = ok && k < N;
-          const double lk = in ? __ldcg(gl + k) : 0.0;
-          const double uk = (in && !wall) ? __ldcg(gu + k) : 0.0;
-          const double llk = (in && rL) ? __ldcg(gll + k) : 0.0;
-          const double uuk = (in && rU) ? __ldcg(guu + k) : 0.0;
-          Rr[t][h] = (RHS && g == 0 && in) ? __ldcg(gr + k) : 0.0;
-          Lr[t][h] = rL ? fma(oL, (uk - llk) * hL, lk) : lk;
-          Ur[t][h] = rU ? fma(oU, (uuk - lk) * hU, uk) : uk;
-          Sr[t][h] = wall ? lk : uk;
+          lk[t][h] = in ? __ldcg(gl + k) : 0.0;
+          uk[t][h] = (in && !wall) ? __ldcg(gu + k) : 0.0;
+          llk[t][h] = (in && el) ? __ldcg(gl - stride * NP + k) : 0.0;
+          uuk[t][h] = (in && eu) ? __ldcg(gu + stride * NP + k) : 0.0;
+          rk[t][h] = (RHS && g == 0 && in) ? __ldcg(rhsf->c + (size_t)Dcu[cc] * NP + k)  /* g == 0: cu is the cell */ : 0.0;
         }
       }
+      // (2) first batch: this lane's parameter records and reconstruction decision
+      if (t0 == 0) {
+        int dec = 0;
+        double aL = 0.0, aU = 0.0;
+        if (valid) {
+          cp = tc::ldp<true>(f.p + cell * 4);
+          P4 pL = cp, pU = cp, pLL = cp, pUU = cp;
+          if (!at_wall) {
+            pL = tc::ldp<true>(f.p + cl * 4);
+            pU = tc::ldp<true>(f.p + cu * 4);
+          }
+          if (rl) pLL = tc::ldp<true>(f.p + (cl - stride) * 4);
+          if (ru) pUU = tc::ldp<true>(f.p + (cu + stride) * 4);
+          branch = at_wall ? B_WALL : B_HALF;
+          lp = pL;
+          rp = pU;
+          if (rl) {
+            const double hl = xc[pl + 1] - xc[pl - 1], offL = 0.5 * dd[pl];
+            P4 w;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) w.v[qq] = pL.v[qq] + offL * ((pU.v[qq] - pLL.v[qq]) / hl);
+            if (w.v[3] > 0.0) {
+              dec |= 1;
+              lp = w;
+              aL = offL / hl;
+            }
+          }
+          if (ru) {
+            const double hu = xc[pu + 1] - xc[pu - 1], offU = -0.5 * dd[pu];
+            P4 w;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) w.v[qq] = pU.v[qq] + offU * ((pUU.v[qq] - pL.v[qq]) / hu);
+            if (w.v[3] > 0.0) {
+              dec |= 2;
+              rp = w;
+              aU = offU / hu;
+            }
+          }
+        }
+        Ddec[lane] = dec;
+        DaL[lane] = aL;
+        DaU[lane] = aU;
+        __syncwarp();
+      }
+      // (3) apply the decisions and transpose
 #pragma unroll
       for (int t = 0; t < B; ++t) {
         const int cc = 8 * q + t0 + t;
-        if (!(fls[t] & 1)) continue;
-        const bool wall = fls[t] & 2;
+        const int fl = Dfl[cc];
+        if (!(fl & 1)) continue;
+        const bool wall = fl & 2;
+        const int dec = Ddec[cc];
+        const double aL = DaL[cc], aU = DaU[cc];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
           const int k = lane + 32 * h;
           if (k < N) {
-            Lb[k * SPV + cc] = Lr[t][h];
-            if (!wall) Ub[k * SPV + cc] = Ur[t][h];
-            if (g == 0) Sb[k * SPV + cc] = Sr[t][h];
-            if (RHS && g == 0) Rb[k * SPV + cc] = Rr[t][h];
+            const double l = lk[t][h], u = uk[t][h];
+            Lb[k * SPV + cc] = (dec & 1) ? fma(aL, u - llk[t][h], l) : l;
+            if (!wall) Ub[k * SPV + cc] = (dec & 2) ? fma(aU, uuk[t][h] - l, u) : u;
+            if (g == 0) Sb[k * SPV + cc] = wall ? l : u;
+            if (RHS && g == 0) Rb[k * SPV + cc] = rk[t][h];
           }
         }
       }
