@@ -161,8 +161,11 @@ int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_
                       momg_report* report, momg_err* err);
 
 /* ---- execution strategy of fast_sweep (same results either way) -------- */
-/* 1 (default): one persistent dataflow kernel per call; 0: one launch per
-   anti-diagonal (simple reference strategy).  Env MOMG_SWEEP=diag selects 0. */
+/* 1 (default): one persistent dataflow kernel per call (band tasks at first
+   order, M <= 5; wavefront items otherwise); 3: persistent wavefront items
+   only; 2: persistent warp-per-cell kernels only; 0: one launch per
+   anti-diagonal (simple reference strategy).  Env MOMG_SWEEP=diag selects 0,
+   MOMG_BAND=0 disables the band tasks. */
 int momg_set_sweep_mode(int mode);
 
 /* ---- instrumentation --------------------------------------------------- */

@@ -1,0 +1,349 @@
+// Band-persistent exact fast sweep, first order, M <= 5, no rhs (k5_band;
+// sweeps with an FAS right-hand side run the wavefront items of split_cell.cuh).
+//
+// fast_sweep_step (single_level.cpp:121-166) visits the cells of each sweep
+// in lexicographic order (i outer, j inner, in the sweep's direction).  In
+// the sweep's rotated frame (ir, jr) a cell depends on the NEW states of
+// (ir-1, jr) and (ir, jr-1) and the OLD (previous sweep) states of (ir+1, jr)
+// and (ir, jr+1): the anti-diagonals d = ir + jr are the wavefronts.
+//
+// A task is one band of 32 rotated columns (ir = 32k + lane) of one sweep,
+// walked diagonal by diagonal by one CTA (the 512-thread split layout of
+// split_cell.cuh: 4 face groups x 4 partitions, lane = cell).  Everything a
+// step needs except one cell is already on chip:
+//   * the new states of diagonal d-1 are the previous step's update output
+//     (V), shifted by one lane for the x-upstream face;
+//   * the old states of diagonals d and d+1 were prefetched one and two
+//     steps earlier (OLD1 / X), by the 12 warps that are idle while face
+//     group 0 runs the cell update;
+//   * only lane 0's x-upstream neighbour comes from band k-1 (HALO), polled
+//     on its per-cell counter during the previous step's update.
+// So the critical path of a step is copies + face phases + update, with no
+// global round trip on it.  Tasks are handed out in (sweep, band) order by
+// an atomic counter: every dependency of a task (band k-1 of the same sweep,
+// any band of earlier sweeps) belongs to an earlier task, which is running
+// or finished, so the schedule cannot deadlock and needs no co-residency.
+// The per-cell counters (rule in sweep_persistent.cuh) still gate every
+// global read, so tasks of consecutive sweeps overlap safely.
+#pragma once
+
+#include "split_cell.cuh"
+
+namespace momg_gpu {
+namespace sp {
+
+struct BandPlan {
+  unsigned* ver;       // per-cell sweep counters (zeroed per launch)
+  unsigned* next;      // task counter (zeroed per launch)
+  int nsweeps;         // <= 16
+  int nbands;          // ceil(nx / 32)
+  int dirs[16];
+  unsigned dirbits;  // dirs[s] = (dirbits >> 2s) & 3 (no runtime-indexed param array)
+  int poll_ns;
+  int exp;  // experiment flags (debug timing only; results invalid when set)
+  unsigned long long* trace;  // optional per-task [8] stamps (debug)
+  long long trace_cap;
+};
+
+template <int M>
+struct BandLayout {
+  static constexpr int N = Gen<M>::N;
+  static constexpr int VEC = N * SPV;
+  // vectors: 0..11 face groups (L, U, F), 12 S, 13 X, 14 OLD1; the update's
+  // V / D are group 1's L / U (update_split)
+  static constexpr int V_V = 3, V_S = 12, V_X = 13, V_OLD1 = 14;
+  static constexpr int PO = 15 * VEC;  // params of OLD1 [33][4]
+  static constexpr int PX = PO + 132;  // params of X [33][4]
+  static constexpr int PV = PX + 132;  // params of V [32][4]
+  static constexpr int HALO = PV + 128;  // band k-1 new state [N] + params [4]
+  static constexpr int HALOP = HALO + N;
+  static constexpr size_t bytes = (size_t)(HALOP + 4) * sizeof(double);
+};
+
+struct BandGeo {
+  int nx, ny, k;
+  bool i_up, j_up;
+  // rotated cell (ir = 32k + slot, jr = dd - ir) -> flat index, or -1
+  __device__ __forceinline__ int cell(int slot, int dd) const {
+    const int ir = 32 * k + slot, jr = dd - ir;
+    if (ir < 0 || ir >= nx || jr < 0 || jr >= ny) return -1;
+    const int i = i_up ? ir : nx - 1 - ir, j = j_up ? jr : ny - 1 - jr;
+    return j * nx + i;
+  }
+};
+
+__device__ __forceinline__ bool band_stop(const DevErr* err) {
+  return *((volatile const int*)&err->code) != 0;
+}
+
+// Warp wi of nw loads slots s0 + wi, s0 + wi + nw, ... (< s0 + ns) of
+// diagonal dd: coefficient records into vec[k * vstride + (slot - s0)] and
+// parameters into prm[(slot - s0) * 4 ..], once the cell's counter reaches
+// `need` (0: no wait).  All of a warp's polls, then all of its loads, are in
+// flight together.
+template <int M, int MAXS>
+__device__ __forceinline__ void band_load(const DevField& fld, const unsigned* ver, const BandGeo& b, int dd,
+                                          int s0, int ns, unsigned need, double* vec, int vstride, double* prm,
+                                          int wi, int nw, DevErr* err, int poll_ns) {
+  constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, H = (N + 31) / 32;
+  static_assert(MAXS <= 32, "one polling lane per slot");
+  constexpr int PR = (4 * MAXS + 31) / 32;  // rounds of parameter loads (4 lanes per slot)
+  const int lane = threadIdx.x & 31;
+  int my_cell = -1;
+  if (lane < MAXS) {
+    const int slot = s0 + wi + lane * nw;
+    if (slot < s0 + ns) my_cell = b.cell(slot, dd);
+  }
+  if (need && my_cell >= 0) {
+    const unsigned* a = ver + my_cell;
+    long long polls = 0;
+    while (ld_relaxed(a) < need) {
+      if (band_stop(err)) break;
+      if (++polls > (1LL << 26)) {
+        tc::raise(err, E_ERROR, W_DEADLOCK, my_cell % b.nx, my_cell / b.nx, (double)need);
+        break;
+      }
+      if (poll_ns) __nanosleep(poll_ns);
+    }
+    (void)ld_acquire(a);
+  }
+  __syncwarp();
+  double r[MAXS][H];
+  double pr[PR];
+#pragma unroll
+  for (int t = 0; t < MAXS; ++t) {
+    const int cl = __shfl_sync(0xffffffffu, my_cell, t);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int kk = lane + 32 * h;
+      r[t][h] = (cl >= 0 && kk < N) ? __ldcg(fld.c + (size_t)cl * NP + kk) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < PR; ++rr) {
+    const int t = (lane + 32 * rr) >> 2;
+    const int cl = __shfl_sync(0xffffffffu, my_cell, t < MAXS ? t : 0);
+    pr[rr] = (t < MAXS && cl >= 0) ? __ldcg(fld.p + (size_t)cl * 4 + (lane & 3)) : 0.0;
+  }
+#pragma unroll
+  for (int t = 0; t < MAXS; ++t) {
+    const int slot = s0 + wi + t * nw;
+    if (slot >= s0 + ns) continue;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int kk = lane + 32 * h;
+      if (kk < N) vec[kk * vstride + (slot - s0)] = r[t][h];
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < PR; ++rr) {
+    const int t = (lane + 32 * rr) >> 2;
+    const int slot = s0 + wi + t * nw;
+    if (t < MAXS && slot < s0 + ns && prm) prm[(slot - s0) * 4 + (lane & 3)] = pr[rr];
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, DevErr* err, BandPlan plan) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int s_task, s_stop;
+  __shared__ unsigned long long s_tr[16];  // debug trace accumulators (thread 0)
+  __shared__ unsigned long long s_ph[4];   // debug: face phase stamps of group 0
+  using LY = BandLayout<M>;
+  constexpr int N = LY::N, VEC = LY::VEC;
+  constexpr int NE = 33 * N;                         // elements of one 33-slot vector
+  constexpr int EPT = (NE + THREADS - 1) / THREADS;  // per thread in the copy phase
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, g = warp / P, q = warp % P, c = tid & 31;
+  const int ntasks = plan.nsweeps * plan.nbands;
+  for (;;) {
+    if (tid == 0) {
+      s_task = (int)atomicAdd(plan.next, 1u);
+      s_stop = band_stop(err);
+    }
+    __syncthreads();
+    const int task = s_task;
+    if (task >= ntasks || s_stop) return;
+    const int s = task / plan.nbands, k = task % plan.nbands;
+    const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
+    BandGeo b;
+    b.nx = f.nx;
+    b.ny = f.ny;
+    b.k = k;
+    b.i_up = dir == 0 || dir == 3;  // kSweepDirs (single_level.cpp:116-117)
+    b.j_up = dir == 0 || dir == 1;
+    const int ir = 32 * k + c;
+    const int dfirst = 32 * k, dlast = min(32 * k + 31, f.nx - 1) + f.ny - 1;
+    const bool tr = plan.trace && 2 * task + 1 < plan.trace_cap && tid == 0;
+    if (tr) {
+      s_tr[0] = gtimer();
+      for (int t = 2; t < 16; ++t) s_tr[t] = 0;
+    }
+    // prologue: OLD1 <- old(dfirst), X <- old(dfirst+1), HALO <- band k-1 at dfirst-1
+    band_load<M, 4>(f, plan.ver, b, dfirst, 0, 33, (unsigned)s, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp,
+                 16, err, plan.poll_ns);
+    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, 33, (unsigned)s, smem + LY::V_X * VEC, SPV, smem + LY::PX,
+                 warp, 16, err, plan.poll_ns);
+    if (k > 0 && warp == 15)
+      band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, (unsigned)s + 1u, smem + LY::HALO, 1, smem + LY::HALOP, 0,
+                   1, err, plan.poll_ns);
+    __syncthreads();
+    if (tr) s_tr[1] = gtimer();
+    for (int d = dfirst; d <= dlast; ++d) {
+      if (tr) s_tr[3] = gtimer();
+      // ---- (A) stage the step's face states.  Sources: OLD1 (own old
+      // states), X (old states of diagonal d+1), V (= L of group 1: new
+      // states of d-1) and HALO.  Every destination except group 1's L is
+      // written at once; those values are held over one barrier because
+      // group 1's L is where V lives.
+      double hold[EPT];
+      {
+        const double* OLD1 = smem + LY::V_OLD1 * VEC;
+        const double* X = smem + LY::V_X * VEC;
+        const double* Vv = smem + LY::V_V * VEC;
+        const double* HALO = smem + LY::HALO;
+        const int gux = b.i_up ? 0 : 1, guy = b.j_up ? 2 : 3;  // upstream face groups
+#pragma unroll
+        for (int r = 0; r < EPT; ++r) {
+          const int e = tid + r * THREADS;
+          hold[r] = 0.0;
+          if (e < NE) {
+            const int kk = e / 33, sl = e - kk * 33;
+            const int o = kk * SPV + sl;
+            const double x = X[o];
+            if (sl < 32) {
+              const double self = OLD1[o];
+              const double xu = sl ? Vv[o - 1] : HALO[kk];
+              const double yu = Vv[o];
+              const double xd = X[o + 1];
+              const int irs = 32 * k + sl, jrs = d - irs;
+              const bool sxu = irs >= 1, sxd = irs + 1 < f.nx, syu = jrs >= 1, syd = jrs + 1 < f.ny;
+              smem[LY::V_S * VEC + o] = self;
+              // face group gg: the neighbour is the lower cell of a low face
+              // (L) and the upper cell of a high face (U); walls take L = self
+#pragma unroll
+              for (int gg = 0; gg < 4; ++gg) {
+                const bool up = gg == ((gg >> 1) == 0 ? gux : guy);
+                const bool has = (gg >> 1) == 0 ? (up ? sxu : sxd) : (up ? syu : syd);
+                const double nbv = (gg >> 1) == 0 ? (up ? xu : xd) : (up ? yu : x);
+                const bool low = (gg & 1) == 0;
+                const double lv = (has && low) ? nbv : self;
+                if (gg != 1) smem[(gg * 3) * VEC + o] = lv;
+                else hold[r] = lv;
+                smem[(gg * 3 + 1) * VEC + o] = low ? self : nbv;
+              }
+            }
+            smem[LY::V_OLD1 * VEC + o] = x;
+          }
+        }
+      }
+      // this lane's parameters and geometry
+      const int jr = d - ir;
+      const bool valid = ir < f.nx && jr >= 0 && jr < f.ny;
+      const int i = valid ? (b.i_up ? ir : f.nx - 1 - ir) : 0;
+      const int j = valid ? (b.j_up ? jr : f.ny - 1 - jr) : 0;
+      P4 cp, lp, rp;
+      int branch;
+      {
+        const int axis = g >> 1;
+        const bool up = g == (axis == 0 ? (b.i_up ? 0 : 1) : (b.j_up ? 2 : 3));
+        const bool has_nb = axis == 0 ? (up ? ir >= 1 : ir + 1 < f.nx) : (up ? jr >= 1 : jr + 1 < f.ny);
+        // neighbour parameters: upstream = new (PV / HALOP), downstream = old (PX)
+        const int off = up ? (axis == 0 ? (c ? LY::PV + (c - 1) * 4 : LY::HALOP) : LY::PV + c * 4)
+                           : LY::PX + (axis == 0 ? c + 1 : c) * 4;
+        P4 nb;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          cp.v[t] = smem[LY::PO + c * 4 + t];
+          nb.v[t] = smem[off + t];
+        }
+        branch = !valid ? B_NONE : (has_nb ? B_HALF : B_WALL);
+        const bool low = (g & 1) == 0;  // low face: L is the neighbour
+        lp = low ? nb : cp;
+        rp = low ? cp : nb;
+      }
+      double dxi = 1.0, dyj = 1.0;
+      if (valid && g == 0) {
+        dxi = f.dx[i];
+        dyj = f.dy[j];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const int e = tid + r * THREADS;
+        if (e < NE) {
+          const int kk = e / 33, sl = e - kk * 33;
+          if (sl < 32) smem[3 * VEC + kk * SPV + sl] = hold[r];
+        }
+      }
+      if (tid < 132) smem[LY::PO + tid] = smem[LY::PX + tid];
+      __syncthreads();
+      if (tr) s_tr[4] += gtimer() - s_tr[3];
+      // ---- (B) face fluxes (face_flux / wall_flux, back into the cell basis)
+      {
+        double* L = smem + (g * 3) * VEC + c;
+        int w;
+        if (g < 2)
+          w = face_core<M, 0>(ctx, g, q, g & 1, branch, W_NONE, lp, rp, cp, L, L + VEC, L + 2 * VEC,
+                             tr ? s_ph : nullptr);
+        else
+          w = face_core<M, 1>(ctx, g, q, g & 1, branch, W_NONE, lp, rp, cp, L, L + VEC, L + 2 * VEC, nullptr);
+        if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, 0.0);
+      }
+      __syncthreads();
+      if (tr) {
+        s_tr[5] += gtimer() - s_tr[3];
+        s_tr[8] += s_ph[1] - s_tr[3];
+        s_tr[9] += s_ph[2] - s_tr[3];
+      }
+      // ---- (C) face group 0: cell update (update_split) and publication of
+      // the step's cells; groups 1-3: prefetch old(d+2) and band k-1's new
+      // cell for the next step
+      if (g == 0) {
+        double bad = 0.0;
+        P4 np = cp;
+        const int w = update_split<M>(f, nullptr, ctx, q, valid, i, j, smem, &bad, cp, dxi, dyj, &np);
+        if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
+        if (tr) s_tr[7] += gtimer() - s_tr[3];
+        if (q == 0) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) smem[LY::PV + c * 4 + t] = np.v[t];
+        }
+        gbar(0);
+        if (q == 0 && valid && w == W_NONE) st_release(plan.ver + (size_t)j * f.nx + i, (unsigned)s + 1u);
+      } else {
+        const int wi = warp - 4;
+        if (d + 1 <= dlast)
+          band_load<M, 4>(f, plan.ver, b, d + 2, 0, 33, (unsigned)s, smem + LY::V_X * VEC, SPV, smem + LY::PX, wi,
+                          12, err, plan.poll_ns);
+        if (k > 0 && wi == 11 && d + 1 <= dlast)
+          band_load<M, 1>(f, plan.ver, b, d, -1, 1, (unsigned)s + 1u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1,
+                          err, plan.poll_ns);
+        if (tid == 128) {
+          s_stop = band_stop(err);
+          if (plan.trace && 2 * task + 1 < plan.trace_cap) s_tr[2] += gtimer() - s_tr[3];
+        }
+      }
+      __syncthreads();
+      if (tr) s_tr[6] += gtimer() - s_tr[3];
+      if (s_stop) return;
+    }
+    if (tr) {
+      unsigned long long* o = plan.trace + (size_t)task * 16;
+      // [loop start, end, steps | s << 20 | k << 28, sums from step start
+      //  to: copies, faces, update, prefetch, step end]
+      o[0] = s_tr[1];
+      o[1] = gtimer();
+      o[2] = (unsigned long long)(dlast - dfirst + 1) | ((unsigned long long)s << 20) | ((unsigned long long)k << 28);
+      o[3] = s_tr[4];
+      o[4] = s_tr[5];
+      o[5] = s_tr[7];
+      o[6] = s_tr[2];
+      o[7] = s_tr[6];
+      for (int t = 8; t < 16; ++t) o[t] = s_tr[t];
+    }
+  }
+}
+
+}  // namespace sp
+}  // namespace momg_gpu

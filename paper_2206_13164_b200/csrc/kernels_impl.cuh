@@ -21,6 +21,7 @@
 #include "sweep_persistent.cuh"
 #include "kernels_v3.cuh"
 #include "split_cell.cuh"
+#include "band_sweep.cuh"
 
 namespace momg_gpu {
 
@@ -353,6 +354,10 @@ template <int M>
 constexpr bool use_split() { return M <= 5; }
 bool split_sweep_enabled();
 unsigned long long* trace_buffer(long long* cap);
+void poll_tuning(int* split_wait, int* poll_ns);
+void band_scratch(momg_field* f, unsigned** ver, unsigned** next);
+bool band_sweep_enabled();
+void set_band_mode(int m);
 const uint32_t* split_schedule(momg_field* f, int nsweeps, const int* dirs, int radius, int seg);
 
 // ---------------------------------------------------- templated launchers
@@ -450,6 +455,31 @@ struct Launch {
             set_smem(sp::k4_sweep<M, 2>, sp::Layout<M>::bytes);
             sattr = true;
           }
+          if (ctx.order == 1 && !rhs && band_sweep_enabled()) {
+            static bool battr = false;
+            if (!battr) {
+              set_smem(sp::k5_band<M>, sp::BandLayout<M>::bytes);
+              battr = true;
+            }
+            sp::BandPlan bp;
+            band_scratch(f, &bp.ver, &bp.next);
+            bp.nsweeps = 4 * iters;
+            bp.nbands = (f->nx + 31) / 32;
+            bp.dirbits = 0;
+            for (int s = 0; s < 16; ++s) {
+              bp.dirs[s] = order[s & 3];
+              bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
+            }
+            int sw = 0;
+            poll_tuning(&sw, &bp.poll_ns);
+            bp.exp = sw;
+            bp.trace = trace_buffer(&bp.trace_cap);
+            int nb = tc_sweep_blocks((const void*)sp::k5_band<M>, sp::BandLayout<M>::bytes, sp::THREADS);
+            if (nb > bp.nsweeps * bp.nbands) nb = bp.nsweeps * bp.nbands;
+            sp::k5_band<M><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp);
+            momg_rt::count_launch(1);
+            return;
+          }
           const tc::SegPlan p16 = tc_seg_plan(f, 32);
           sp::SegPlan32 plan;
           plan.diag_lo = p16.diag_lo;
@@ -457,9 +487,14 @@ struct Launch {
           plan.ver = p16.ver;
           plan.nd = p16.nd;
           plan.nsweeps = 4 * iters;
-          for (int s = 0; s < 16; ++s) plan.dirs[s] = order[s & 3];
+          plan.dirbits = 0;
+          for (int s = 0; s < 16; ++s) {
+            plan.dirs[s] = order[s & 3];
+            plan.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
+          }
           plan.items = split_schedule(f, plan.nsweeps, plan.dirs, ctx.order == 2 ? 2 : 1, 32);
           plan.trace = trace_buffer(&plan.trace_cap);
+          poll_tuning(&plan.split_wait, &plan.poll_ns);
           const void* kern = ctx.order == 2 ? (const void*)sp::k4_sweep<M, 2> : (const void*)sp::k4_sweep<M, 1>;
           int nb = tc_sweep_blocks(kern, sp::Layout<M>::bytes, sp::THREADS);
           DevField fa = fd, ra = rd;

@@ -315,6 +315,7 @@ bool persistent_sweep_enabled() {
 }
 void set_sweep_mode(int m) { g_sweep_mode = m; }
 void set_split_mode(int m);
+void set_band_mode(int m);
 void set_trace(long long cap);
 long long read_trace(unsigned long long* host, long long n);
 
@@ -458,6 +459,36 @@ long long read_trace(unsigned long long* host, long long n) {
   cudaMemcpy(host, g_trace, n * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return n;
 }
+
+// persistent-sweep polling policy (MOMG_POLL="split,ns"; tuning/debug)
+void poll_tuning(int* split_wait, int* poll_ns) {
+  static int sw = -1, ns = 0;
+  if (sw < 0) {
+    sw = 0;
+    if (const char* e = std::getenv("MOMG_POLL")) std::sscanf(e, "%d,%d", &sw, &ns);
+  }
+  *split_wait = sw;
+  *poll_ns = ns;
+}
+
+void band_scratch(momg_field* f, unsigned** ver, unsigned** next) {
+  if (!f->sweep_ver) cudaMalloc(&f->sweep_ver, (size_t)f->nx * f->ny * sizeof(unsigned));
+  if (!f->band_next) cudaMalloc(&f->band_next, 64);
+  cudaMemsetAsync(f->sweep_ver, 0, (size_t)f->nx * f->ny * sizeof(unsigned), momg_rt::stream());
+  cudaMemsetAsync(f->band_next, 0, 64, momg_rt::stream());
+  *ver = f->sweep_ver;
+  *next = f->band_next;
+}
+
+static int g_band = -1;
+bool band_sweep_enabled() {
+  if (g_band < 0) {
+    const char* e = std::getenv("MOMG_BAND");
+    g_band = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  return g_band == 1;
+}
+void set_band_mode(int m) { g_band = m; }
 
 static int g_split = -1;
 bool split_sweep_enabled() {
@@ -618,6 +649,7 @@ void field_free(momg_field* f) {
     delete f->schedule;
   }
   cudaFree(f->sweep_ver);
+  cudaFree(f->band_next);
   delete f;
 }
 
@@ -675,9 +707,10 @@ long long momg_debug_trace_read(unsigned long long* host, long long n) {
   return momg_gpu::read_trace(host, n);
 }
 int momg_set_sweep_mode(int mode) {
-  if (mode < 0 || mode > 2) return MOMG_ERR_ARG;
+  if (mode < 0 || mode > 3) return MOMG_ERR_ARG;
   momg_gpu::set_sweep_mode(mode == 0 ? 0 : 1);
   momg_gpu::set_split_mode(mode == 2 ? 0 : 1);
+  momg_gpu::set_band_mode(mode == 1 ? 1 : 0);
   return MOMG_OK;
 }
 

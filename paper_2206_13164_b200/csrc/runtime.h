@@ -19,6 +19,7 @@ struct momg_field {
   double* dgrid = nullptr;  // dx | dy | xc | yc
   uint32_t* sweep_order = nullptr;  // persistent sweep: diagonal order (lazy)
   unsigned* sweep_ver = nullptr;    // persistent sweep: per-cell counters (lazy)
+  unsigned* band_next = nullptr;    // band sweep: task counter (lazy)
   int* seg_plan = nullptr;          // thread-granular sweep: diag_lo | seg_start (lazy)
   int* seg_plan32 = nullptr;        // split sweep (32-cell segments)
   struct Schedule* schedule = nullptr;  // split sweep: cached dependency-level item order

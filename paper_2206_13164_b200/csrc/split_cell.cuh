@@ -86,6 +86,20 @@ __device__ __forceinline__ void pass(int q, int d, double* v, const double* c) {
 #undef SP_PASS
 }
 
+// both vectors' passes of partition q with every load issued first
+template <int M>
+__device__ __forceinline__ void pass_two(int q, int d, double* a, const double* ca, bool acta, double* b,
+                                         const double* cb, bool actb) {
+#define SP_PASS2(Q)                                                    \
+  {                                                                    \
+    if (d == 0) Split<M, P>::pass20_##Q(a, ca, acta, b, cb, actb);     \
+    else if (d == 1) Split<M, P>::pass21_##Q(a, ca, acta, b, cb, actb); \
+    else Split<M, P>::pass22_##Q(a, ca, acta, b, cb, actb);            \
+  }
+  SP_DISPATCH(q, SP_PASS2)
+#undef SP_PASS2
+}
+
 // Projection (projection.hpp:64-89) of the vectors of this cell, split over
 // the group's partitions: every thread of the group runs the three passes
 // and barriers; `active` selects whether this cell's vector is touched.
@@ -97,8 +111,9 @@ __device__ __forceinline__ void project2(int g, int q, double* a, const P4& af, 
     double ca[M + 1], cb[M + 1];
     coeffs<M>(af, at, d, ca);
     coeffs<M>(bf, bt, d, cb);
-    if (act_a) pass<M>(q, d, a, ca);
-    if (act_b) pass<M>(q, d, b, cb);
+    if (act_a && act_b) pass_two<M>(q, d, a, ca, true, b, cb, true);
+    else if (act_a) pass<M>(q, d, a, ca);
+    else if (act_b) pass<M>(q, d, b, cb);
     gbar(g);
   }
 }
@@ -385,6 +400,87 @@ __device__ __forceinline__ unsigned long long gtimer0() {
   return t;
 }
 
+// Phases 1-4 of one face group on states already staged in L / U
+// (face_flux, flux.cpp:77-132, and the back projection of spatial.cpp:118-125).
+// branch: B_HALF (interior face, lp / rp the face states' bases) or B_WALL
+// (L = the cell state in basis cp); invalid lanes pass B_NONE.
+template <int M, int AXIS>
+__device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, bool high, int branch, int fail,
+                                         const P4& lp, const P4& rp, const P4& cp, double* L, double* U,
+                                         double* F, unsigned long long* stamp) {
+  P4 fp{};
+  // ---- phase 1: wave-speed bounds and branch (flux.cpp:77-97)
+  P4 wb{};
+  double rs = 1.0;
+  if (branch == B_WALL) {
+    // constant indices only: a runtime index would copy ctx to local memory
+    wb.v[AXIS == 0 ? 1 : 0] = high ? ctx.wall_speed[2 * AXIS + 1] : ctx.wall_speed[2 * AXIS];
+    wb.v[3] = high ? ctx.wall_theta[2 * AXIS + 1] : ctx.wall_theta[2 * AXIS];
+    if (!(wb.v[3] > 0.0)) {
+      fail = W_PROJ_SPREAD;
+      branch = B_NONE;
+    } else {
+      rs = sqrt(wb.v[3]);
+    }
+  } else if (branch == B_HALF) {
+    const double ul = rep_u32(L, lp, AXIS), ur = rep_u32(U, rp, AXIS);
+    const double cl = ctx.c_bound * sqrt(rep_theta32(L, lp));
+    const double cr = ctx.c_bound * sqrt(rep_theta32(U, rp));
+    const double lminus = tc::smin(ul - cl, ur - cr);
+    const double lplus = tc::smax(ul + cl, ur + cr);
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) fp.v[qq] = 0.5 * (lp.v[qq] + rp.v[qq]);
+    if (!(fp.v[3] > 0.0)) {
+      fail = W_PROJ_SPREAD;
+      branch = B_NONE;
+    } else if (lminus >= 0.0) {
+      branch = B_FULL_L;
+    } else if (lplus <= 0.0) {
+      branch = B_FULL_R;
+    }
+    rs = fp.v[3] > 0.0 ? sqrt(fp.v[3]) : 1.0;
+  }
+  // ---- phase 2: project the state(s) into the face (or wall) basis
+  {
+    const bool wall = branch == B_WALL;
+    project2<M>(g, q, L, wall ? cp : lp, wall ? wb : fp, wall || branch == B_HALF || branch == B_FULL_L,
+                U, rp, fp, branch == B_HALF || branch == B_FULL_R);
+  }
+  if (stamp) stamp[1] = gtimer0();
+  // ---- phase 3: flux in the face basis into F (per-partition K columns)
+  double kin0[M + 1];
+  {
+    const double un = branch == B_WALL ? 0.0 : fp.v[AXIS];
+#define SP_FQ(Q) flux_q<M, AXIS, Q>(branch, high, un, rs, fp, L, U, F, kin0)
+    SP_DISPATCH(q, SP_FQ)
+#undef SP_FQ
+  }
+  gbar(g);
+  if (stamp) stamp[2] = gtimer0();
+  // wall closure: density of the incoming wall Maxwellian (flux.cpp:119-129)
+  if (branch == B_WALL && q == 0) {
+    const double in0 = kin0[0];
+    const double wall_rho = in0 == 0.0 ? 0.0 : -F[0] / in0;
+    if (in0 == 0.0) {
+      fail = W_WALL_DEGEN;
+    } else if (!(wall_rho > 0.0)) {
+      fail = W_WALL_RHO;
+    } else {
+#pragma unroll
+      for (int p = 1; p <= M; ++p) {
+        const int k = AXIS == 0 ? flat3(p, 0, 0) : flat3(0, p, 0);
+        F[k * SPV] = fma(wall_rho, kin0[p], F[k * SPV]);
+      }
+      F[0] = 0.0;
+    }
+  }
+  gbar(g);
+  // ---- phase 4: flux back into the cell basis (in F)
+  const P4 from = branch == B_WALL ? wb : fp;
+  project2<M>(g, q, F, from, cp, branch != B_NONE, U, cp, cp, false);
+  return fail;
+}
+
 template <int M, int ORDER, int AXIS, bool RHS>
 __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, int g, int q, bool valid,
                                           int i, int j, double* L, double* U, double* F, double* SB,
@@ -538,75 +634,7 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
   }
   gbar(g);
   if (stamp) stamp[0] = gtimer0();
-  // ---- phase 1: wave-speed bounds and branch (flux.cpp:77-97)
-  P4 wb{};
-  double rs = 1.0;
-  if (branch == B_WALL) {
-    const int w = AXIS == 0 ? (high ? 1 : 0) : (high ? 3 : 2);
-    wb.v[AXIS == 0 ? 1 : 0] = ctx.wall_speed[w];
-    wb.v[3] = ctx.wall_theta[w];
-    if (!(wb.v[3] > 0.0)) {
-      fail = W_PROJ_SPREAD;
-      branch = B_NONE;
-    } else {
-      rs = sqrt(wb.v[3]);
-    }
-  } else if (branch == B_HALF) {
-    const double ul = rep_u32(L, lp, AXIS), ur = rep_u32(U, rp, AXIS);
-    const double cl = ctx.c_bound * sqrt(rep_theta32(L, lp));
-    const double cr = ctx.c_bound * sqrt(rep_theta32(U, rp));
-    const double lminus = tc::smin(ul - cl, ur - cr);
-    const double lplus = tc::smax(ul + cl, ur + cr);
-#pragma unroll
-    for (int qq = 0; qq < 4; ++qq) fp.v[qq] = 0.5 * (lp.v[qq] + rp.v[qq]);
-    if (!(fp.v[3] > 0.0)) {
-      fail = W_PROJ_SPREAD;
-      branch = B_NONE;
-    } else if (lminus >= 0.0) {
-      branch = B_FULL_L;
-    } else if (lplus <= 0.0) {
-      branch = B_FULL_R;
-    }
-    rs = fp.v[3] > 0.0 ? sqrt(fp.v[3]) : 1.0;
-  }
-  // ---- phase 2: project the state(s) into the face (or wall) basis
-  {
-    const bool wall = branch == B_WALL;
-    project2<M>(g, q, L, wall ? cp : lp, wall ? wb : fp, wall || branch == B_HALF || branch == B_FULL_L,
-                U, rp, fp, branch == B_HALF || branch == B_FULL_R);
-  }
-  if (stamp) stamp[1] = gtimer0();
-  // ---- phase 3: flux in the face basis into F (per-partition K columns)
-  double kin0[M + 1];
-  {
-    const double un = branch == B_WALL ? 0.0 : fp.v[AXIS];
-#define SP_FQ(Q) flux_q<M, AXIS, Q>(branch, high, un, rs, fp, L, U, F, kin0)
-    SP_DISPATCH(q, SP_FQ)
-#undef SP_FQ
-  }
-  gbar(g);
-  if (stamp) stamp[2] = gtimer0();
-  // wall closure: density of the incoming wall Maxwellian (flux.cpp:119-129)
-  if (branch == B_WALL && q == 0) {
-    const double in0 = kin0[0];
-    const double wall_rho = in0 == 0.0 ? 0.0 : -F[0] / in0;
-    if (in0 == 0.0) {
-      fail = W_WALL_DEGEN;
-    } else if (!(wall_rho > 0.0)) {
-      fail = W_WALL_RHO;
-    } else {
-#pragma unroll
-      for (int p = 1; p <= M; ++p) {
-        const int k = AXIS == 0 ? flat3(p, 0, 0) : flat3(0, p, 0);
-        F[k * SPV] = fma(wall_rho, kin0[p], F[k * SPV]);
-      }
-      F[0] = 0.0;
-    }
-  }
-  gbar(g);
-  // ---- phase 4: flux back into the cell basis (in F)
-  const P4 from = branch == B_WALL ? wb : fp;
-  project2<M>(g, q, F, from, cp, branch != B_NONE, U, cp, cp, false);
+  fail = face_core<M, AXIS>(ctx, g, q, high, branch, fail, lp, rp, cp, L, U, F, stamp);
   *cp_out = cp;
   return fail;
 }
@@ -618,7 +646,7 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
 template <int M>
 __device__ __forceinline__ int update_split(const DevField& f, const DevField* rhs, const DevCtx& ctx,
                                             int q, bool valid, int i, int j, double* base, double* bad,
-                                            P4 cp) {
+                                            P4 cp, double dxi, double dyj, P4* new_p = nullptr) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, VEC = Layout<M>::VEC;
   const int c = threadIdx.x & 31;
   double* S = base + 12 * VEC + c;      // SB (staged in the face phase)
@@ -641,7 +669,7 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
       fail = W_DT_THETA;
     } else {
       const double cc = ctx.cfl_c_bound * sqrt(cp.v[3]);
-      dt = ctx.cfl / ((fabs(cp.v[0]) + cc) / f.dx[i] + (fabs(cp.v[1]) + cc) / f.dy[j]);
+      dt = ctx.cfl / ((fabs(cp.v[0]) + cc) / dxi + (fabs(cp.v[1]) + cc) / dyj);
       const double rho = S[0];
       if (!(rho > 0.0)) fail = W_MACRO_RHO;
       else if (ctx.collision == 1) fail = W_ES_UNSUPPORTED;
@@ -658,7 +686,7 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
   if (rhs) project2<M>(0, q, RH, rp, cp, valid && fail == W_NONE, V, cp, cp, false);
   const bool ok0 = valid && fail == W_NONE;
   if (ok0) {
-    const double idx = 1.0 / f.dx[i], idy = 1.0 / f.dy[j];
+    const double idx = 1.0 / dxi, idy = 1.0 / dyj;
     const int shk = ctx.collision == 2;
     const double shw = ctx.shakhov_w;
     const bool hr = rhs != nullptr;
@@ -758,6 +786,7 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
     }
     __threadfence();
   }
+  if (new_p) *new_p = prm;
   return (valid && !good && fail == W_NONE) ? W_DT_HALVING : fail;
 }
 
@@ -770,8 +799,11 @@ struct SegPlan32 {
   int nd;
   int nsweeps;            // <= 16
   int dirs[16];
+  unsigned dirbits;       // dirs[s] = (dirbits >> 2s) & 3 (no runtime-indexed param array)
   unsigned long long* trace;  // optional [item][4] %globaltimer stamps (debug)
   long long trace_cap;
+  int split_wait;  // 1: each face group waits only for its own stencil
+  int poll_ns;     // back-off between failed polls (0: spin)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -807,41 +839,58 @@ __global__ void __launch_bounds__(THREADS, 1) k4_sweep(DevField f, DevField rhs,
     const int ii = plan.diag_lo[d] + seg * 32 + c;
     const bool valid = ii <= dhi;
     const int jj = d - ii;
-    const int dir = plan.dirs[s];
+    const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
     const bool i_up = dir == 0 || dir == 3, j_up = dir == 0 || dir == 1;  // kSweepDirs
     const int i = valid ? (i_up ? ii : f.nx - 1 - ii) : 0;
     const int j = valid ? (j_up ? jj : f.ny - 1 - jj) : 0;
-    // dependency wait (rule in sweep_persistent.cuh): partition 0 of each face
-    // group polls its face's neighbours, group 0 partition 1 the cell itself
-    if (valid && (q == 0 || (g == 0 && q == 1))) {
+    // dependency wait (rule in sweep_persistent.cuh), per face group: the
+    // group polls exactly the cells its face stencil reads -- partition 1
+    // the cell itself, partition 0 the others (order 1: the face neighbour;
+    // order 2 also the reconstruction neighbours, spatial.cpp:34-50) -- and
+    // only the group's own barrier follows.  At first order the high-face
+    // groups (1, 3) read previous-sweep values only, so they usually start at
+    // once and leave the SM to the low-face groups on the critical path.
+    // Polls spin on relaxed loads; success is confirmed with acquire loads.
+    if (valid && (q == 0 || (q == 1 && (plan.split_wait || g == 0)))) {
       const int axis = g >> 1, side = g & 1;
-      bool ok = false;
+      constexpr int NOFF = ORDER == 2 ? 3 : 1;
       long long polls = 0;
-      while (!ok) {
-        ok = true;
-        if (q == 1) {
-          if (ld_acquire(plan.ver + j * f.nx + i) < (unsigned)s) ok = false;
-        } else {
+      for (int pass = 0; pass < 2; ++pass) {  // 0: relaxed spin, 1: acquire confirm
+        bool ok = false;
+        while (!ok) {
+          ok = true;
+          if (q == 1) {
+            const unsigned* a = plan.ver + j * f.nx + i;
+            if ((pass ? ld_acquire(a) : ld_relaxed(a)) < (unsigned)s) ok = false;
+          } else {
 #pragma unroll
-          for (int dist = 1; dist <= radius; ++dist) {
-            const int ni = axis == 0 ? (side ? i + dist : i - dist) : i;
-            const int nj = axis == 1 ? (side ? j + dist : j - dist) : j;
-            if (ni >= 0 && ni < f.nx && nj >= 0 && nj < f.ny) {
-              const bool before = axis == 0 ? (i_up ? ni < i : ni > i) : (j_up ? nj < j : nj > j);
-              if (ld_acquire(plan.ver + nj * f.nx + ni) < (unsigned)s + (before ? 1u : 0u)) ok = false;
+            for (int t = 0; t < NOFF; ++t) {
+              const int o = side ? (t == 0 ? 1 : t == 1 ? 2 : -1) : (t == 0 ? -1 : t == 1 ? -2 : 1);
+              const int ni = axis == 0 ? i + o : i;
+              const int nj = axis == 1 ? j + o : j;
+              if (ni >= 0 && ni < f.nx && nj >= 0 && nj < f.ny) {
+                const bool before = axis == 0 ? (i_up ? ni < i : ni > i) : (j_up ? nj < j : nj > j);
+                const unsigned* a = plan.ver + nj * f.nx + ni;
+                if ((pass ? ld_acquire(a) : ld_relaxed(a)) < (unsigned)s + (before ? 1u : 0u)) ok = false;
+              }
             }
           }
-        }
-        if (!ok) {
-          if (*((volatile const int*)&err->code) != 0) break;
-          if (++polls > (1LL << 26)) {  // deadlock guard: fail loudly, never hang
-            tc::raise(err, E_ERROR, W_DEADLOCK, i, j, (double)s);
-            break;
+          if (!ok) {
+            if (*((volatile const int*)&err->code) != 0) break;
+            if (++polls > (1LL << 26)) {  // deadlock guard: fail loudly, never hang
+              tc::raise(err, E_ERROR, W_DEADLOCK, i, j, (double)s);
+              break;
+            }
+            if (plan.poll_ns) __nanosleep(plan.poll_ns);
           }
         }
+        if (!ok) break;
       }
     }
-    __syncthreads();
+    if (plan.split_wait)
+      gbar(g);
+    else
+      __syncthreads();
     if (tr) plan.trace[item * 8 + 1] = gtimer();
     unsigned long long* st = tr ? plan.trace + item * 8 + 4 : nullptr;
     double* SB = smem + 12 * VEC + c;
@@ -860,7 +909,8 @@ __global__ void __launch_bounds__(THREADS, 1) k4_sweep(DevField f, DevField rhs,
     w = W_NONE;
     double bad = 0.0;
     if (g == 0) {
-      w = update_split<M>(f, has_rhs ? &rhs : nullptr, ctx, q, valid, i, j, smem, &bad, cpv);
+      w = update_split<M>(f, has_rhs ? &rhs : nullptr, ctx, q, valid, i, j, smem, &bad, cpv,
+                          valid ? f.dx[i] : 1.0, valid ? f.dy[j] : 1.0);
       if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
     }
     __syncthreads();

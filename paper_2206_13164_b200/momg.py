@@ -33,7 +33,7 @@ from enum import IntEnum
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libmomg_gpu.so")
+LIB_PATH = os.environ.get("MOMG_GPU_LIB") or os.path.join(HERE, "_lib", "libmomg_gpu.so")  # env: A/B builds
 CSRC = os.path.join(HERE, "csrc")
 
 
@@ -498,8 +498,10 @@ def cavity_context(M: int, space_order: int = 1, model: CollisionKind = Collisio
 
 
 def set_sweep_mode(mode: str) -> None:
-    """'persistent' (default: one dataflow kernel per fast_sweep_step) or
-    'diag' (one launch per anti-diagonal).  Results are identical."""
-    rc = lib().momg_set_sweep_mode({"diag": 0, "persistent": 1}[mode])
+    """'persistent' (default: one dataflow kernel per fast_sweep_step; band
+    tasks at first order), 'items' (persistent wavefront items only), 'warp'
+    (persistent warp-per-cell kernels) or 'diag' (one launch per
+    anti-diagonal).  Results are identical up to rounding."""
+    rc = lib().momg_set_sweep_mode({"diag": 0, "persistent": 1, "warp": 2, "items": 3}[mode])
     if rc:
         raise ValueError(mode)

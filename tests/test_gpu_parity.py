@@ -40,7 +40,7 @@ def rel_res(got, want):
     return float(np.max(np.abs(got - want) / scale))
 
 
-@pytest.fixture(params=["persistent", "diag"])
+@pytest.fixture(params=["persistent", "items", "diag"])
 def sweep_mode(request):
     momg.set_sweep_mode(request.param)
     yield request.param
@@ -107,6 +107,36 @@ def test_sweep_order_and_rhs(order, sweep_mode):
     gc, gp = f.download()
     assert rel_field(gc, wc) < TOL
     assert np.max(np.abs(gp - wp)) < TOL
+
+
+# Band tasks (first order, M <= 5): grids wider than one 32-column band, so
+# the inter-band halo, partial bands and every sweep direction are exercised.
+BAND_CASES = [
+    # (M, model, nx, ny, sweep order, with rhs)
+    (5, BGK, 70, 37, (0, 1, 2, 3), False),
+    (3, SHAKHOV, 33, 5, (2, 0, 3, 1), True),
+    (4, BGK, 64, 40, (1, 1, 3, 3), True),
+    (5, SHAKHOV, 40, 66, (3, 2, 1, 0), True),
+]
+
+
+@pytest.mark.parametrize("M,model,nx,ny,order,with_rhs", BAND_CASES)
+def test_band_sweep_parity(M, model, nx, ny, order, with_rhs):
+    g, octx, c, p = _setup(M, 1, model, nx, ny, True)
+    rhs_h = None
+    if with_rhs:
+        rc = c * 1e-3
+        rp = p.copy(); rp[:, 0] += 0.01; rp[:, 3] *= 1.02
+        rhs_h = (rc, rp)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    rhs = momg.CellField.from_host(mgrid(g), M, *rhs_h) if with_rhs else None
+    wc, wp = c, p
+    for it in range(2):
+        wc, wp, _ = O.fast_sweep(octx, g, wc, wp, rhs=rhs_h, sweep_order=list(order))
+        momg.fast_sweep_step(f, rhs, mctx(octx), None, order)
+        gc, gp = f.download()
+        assert rel_field(gc, wc) < TOL, f"iteration {it}"
+        assert np.max(np.abs(gp - wp)) < TOL
 
 
 @pytest.mark.parametrize("M", [3, 5, 6, 8])

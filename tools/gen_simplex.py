@@ -185,7 +185,9 @@ def emit_split(M, P):
     L = []
     w = L.append
     w(f"template <>\nstruct Split<{M}, {P}> {{")
-    # passes: out-of-place src -> dst (every element written exactly once)
+    # in-place axis passes of partition q: every load of the partition is
+    # issued before the first store, so the smem round trips overlap (loads
+    # and stores to different pencils would otherwise serialise)
     for d in range(3):
         others = [o for o in range(3) if o != d]
         pencils = {}
@@ -194,21 +196,36 @@ def emit_split(M, P):
         costs = {k: len(v) * (len(v) + 1) // 2 + 2 * len(v) for k, v in pencils.items()}
         parts = lpt(costs, P)
         for q in range(P):
-            w(f"  static __device__ __forceinline__ void pass{d}_{q}(double* __restrict__ v, const double* c) {{")
+            mine = []
             for key in parts[q]:
                 members = sorted(pencils[key], key=lambda a: a[d])
                 ks = [pos[a] for a in members]
-                if len(ks) < 2:
-                    continue
-                w("    {")
-                for j, k in enumerate(ks):
-                    w(f"      const double f{j} = v[{k} * SPV];")
-                for j in range(len(ks) - 1, 0, -1):
-                    expr = f"f{j}"
-                    for n in range(1, j + 1):
-                        expr = f"fma(c[{n}], f{j - n}, {expr})"
-                    w(f"      v[{ks[j]} * SPV] = {expr};")
-                w("    }")
+                if len(ks) >= 2:
+                    mine.append(ks)
+
+            def body(vec, cn, tag, guard=None):
+                out = []
+                for t, ks in enumerate(mine):
+                    for j, k in enumerate(ks):
+                        out.append(f"    const double {tag}{t}_{j} = {vec}[{k} * SPV];")
+                for t, ks in enumerate(mine):
+                    for j in range(len(ks) - 1, 0, -1):
+                        expr = f"{tag}{t}_{j}"
+                        for n in range(1, j + 1):
+                            expr = f"fma({cn}[{n}], {tag}{t}_{j - n}, {expr})"
+                        st = f"{vec}[{ks[j]} * SPV] = {expr};"
+                        out.append(f"    if ({guard}) {st}" if guard else f"    {st}")
+                return out
+            w(f"  static __device__ __forceinline__ void pass{d}_{q}(double* __restrict__ v, const double* c) {{")
+            L.extend(body("v", "c", "f"))
+            w("  }")
+            # two vectors at once (project2): all loads of both first
+            w(f"  static __device__ __forceinline__ void pass2{d}_{q}(double* __restrict__ a, const double* ca, bool acta, "
+              f"double* __restrict__ b, const double* cb, bool actb) {{")
+            la = body("a", "ca", "fa", "acta")
+            lb = body("b", "cb", "fb", "actb")
+            nla = sum(len(ks) for ks in mine)
+            L.extend(la[:nla] + lb[:nla] + la[nla:] + lb[nla:])
             w("  }")
     # half sums split by the normal index p
     for a in range(2):

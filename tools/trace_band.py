@@ -1,0 +1,46 @@
+"""Per-task timeline of the band-persistent sweep (debug trace).
+
+usage: python tools/trace_band.py [n] [M]
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2206_13164_b200 import momg  # noqa: E402
+from paper_2206_13164_b200.synthetic import c5_field  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+M = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+g = momg.Grid2D.uniform(n, n)
+ctx = momg.cavity_context(M, 1, knudsen=0.1, lid=0.0)
+c, p = c5_field(n, n, M, seed=1)
+f = momg.CellField.from_host(g, M, c, p)
+momg.fast_sweep_step(f, None, ctx)
+L = momg.lib()
+nb = (n + 31) // 32
+cap = 4 * nb
+L.momg_debug_trace(C.c_longlong(2 * cap))
+momg.fast_sweep_step(f, None, ctx)
+buf = np.zeros((cap, 16), dtype=np.uint64)
+got = L.momg_debug_trace_read(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_longlong(2 * cap)) // 2
+t = buf[:got].astype(np.float64)
+steps = (buf[:got, 2] & 0xfffff).astype(np.float64)
+sk = [(int(v >> 20) & 0xff, int(v >> 28)) for v in buf[:got, 2]]
+t0 = t[:, 0].min()
+S = np.sum(steps)
+print(f"tasks {got}  span {(t[:, 1].max() - t0) / 1e3:.1f} us")
+print("per-step means, us from step start: copies %.2f  faces %.2f  update %.2f  prefetch %.2f  end %.2f;"
+      "  loop time/step %.2f" % tuple([np.sum(t[:, q]) / S / 1e3 for q in (3, 4, 5, 6, 7)]
+                                      + [np.sum(t[:, 1] - t[:, 0]) / S / 1e3]))
+print("face detail (group 0), us from step start: projected %.2f  flux %.2f" % tuple(
+    np.sum(t[:, q]) / S / 1e3 for q in (8, 9)))
+print(" task  s   k  loop(us)  end(us)  steps  us/step")
+rows = [int(x) for x in os.environ.get('ROWS', '').split(',') if x] or (list(range(0, min(4, got))) + list(range(nb - 2, nb + 2)) + list(range(got - 3, got)))
+for r in rows:
+    if 0 <= r < got:
+        s, k = sk[r]
+        print(f"{r:5d} {s:2d} {k:3d} {(t[r,0]-t0)/1e3:8.1f} {(t[r,1]-t0)/1e3:8.1f} "
+              f"{int(steps[r]):6d} {(t[r,1]-t[r,0])/steps[r]/1e3:8.2f}")
