@@ -72,6 +72,10 @@ struct BandGeo {
   }
 };
 
+// back-off of the prologue poll (a task may wait for half a sweep; tight
+// spinning by the waiting CTAs would load the L2 the running tasks use)
+constexpr int kPrologueSleepNs = 512;
+
 __device__ __forceinline__ bool band_stop(const DevErr* err) {
   return *((volatile const int*)&err->code) != 0;
 }
@@ -179,16 +183,37 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       s_tr[0] = gtimer();
       for (int t = 2; t < 16; ++t) s_tr[t] = 0;
     }
-    // prologue: OLD1 <- old(dfirst), X <- old(dfirst+1), HALO <- band k-1 at dfirst-1
-    band_load<M, 4>(f, plan.ver, b, dfirst, 0, 33, (unsigned)s, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp,
-                 16, err, plan.poll_ns);
-    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, 33, (unsigned)s, smem + LY::V_X * VEC, SPV, smem + LY::PX,
-                 warp, 16, err, plan.poll_ns);
-    if (k > 0 && warp == 15)
-      band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, (unsigned)s + 1u, smem + LY::HALO, 1, smem + LY::HALOP, 0,
-                   1, err, plan.poll_ns);
+    // prologue: warp 0 alone waits (with back-off) for the cells of the
+    // first two diagonals and band k-1's halo cell, then every warp loads
+    // OLD1 <- old(dfirst), X <- old(dfirst+1), HALO <- band k-1 at dfirst-1
+    if (warp == 0) {
+      for (int e = c; e < 67; e += 32) {
+        const int cl = e < 66 ? b.cell(e % 33, dfirst + e / 33) : (k > 0 ? b.cell(-1, dfirst - 1) : -1);
+        const unsigned need = e < 66 ? (unsigned)s : (unsigned)s + 1u;
+        if (cl >= 0 && need) {
+          long long polls = 0;
+          while (ld_relaxed(plan.ver + cl) < need) {
+            if (band_stop(err)) break;
+            if (++polls > (1LL << 26)) {
+              tc::raise(err, E_ERROR, W_DEADLOCK, cl % f.nx, cl / f.nx, (double)need);
+              break;
+            }
+            __nanosleep(kPrologueSleepNs);
+          }
+          (void)ld_acquire(plan.ver + cl);
+        }
+      }
+    }
     __syncthreads();
-    if (tr) s_tr[1] = gtimer();
+    band_load<M, 4>(f, plan.ver, b, dfirst, 0, 33, 0u, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp, 16, err, 0);
+    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, 33, 0u, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err, 0);
+    if (k > 0 && warp == 15)
+      band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, 0u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1, err, 0);
+    __syncthreads();
+    if (tr) {
+      s_tr[1] = gtimer();
+      s_tr[10] = clock64();
+    }
     for (int d = dfirst; d <= dlast; ++d) {
       if (tr) s_tr[3] = gtimer();
       // ---- (A) stage the step's face states.  Sources: OLD1 (own old
@@ -282,12 +307,8 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       // ---- (B) face fluxes (face_flux / wall_flux, back into the cell basis)
       {
         double* L = smem + (g * 3) * VEC + c;
-        int w;
-        if (g < 2)
-          w = face_core<M, 0>(ctx, g, q, g & 1, branch, W_NONE, lp, rp, cp, L, L + VEC, L + 2 * VEC,
-                             tr ? s_ph : nullptr);
-        else
-          w = face_core<M, 1>(ctx, g, q, g & 1, branch, W_NONE, lp, rp, cp, L, L + VEC, L + 2 * VEC, nullptr);
+        const int w = face_core<M>(ctx, g, q, g >> 1, g & 1, branch, W_NONE, lp, rp, cp, L, L + VEC, L + 2 * VEC,
+                                   tr && g == 0 ? s_ph : nullptr);
         if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, 0.0);
       }
       __syncthreads();
@@ -296,23 +317,35 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         s_tr[8] += s_ph[1] - s_tr[3];
         s_tr[9] += s_ph[2] - s_tr[3];
       }
-      // ---- (C) face group 0: cell update (update_split) and publication of
-      // the step's cells; groups 1-3: prefetch old(d+2) and band k-1's new
-      // cell for the next step
+      // ---- (C) face group 0: cell update (update_split); groups 1-3:
+      // publish the previous step's cells, prefetch old(d+2) and band k-1's
+      // new cell for the next step
       if (g == 0) {
         double bad = 0.0;
         P4 np = cp;
-        const int w = update_split<M>(f, nullptr, ctx, q, valid, i, j, smem, &bad, cp, dxi, dyj, &np);
+        const int w = update_split<M>(f, nullptr, ctx, q, valid, i, j, smem, &bad, cp, dxi, dyj, &np,
+                                      tr ? s_tr + 3 : nullptr);
         if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
         if (tr) s_tr[7] += gtimer() - s_tr[3];
         if (q == 0) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) smem[LY::PV + c * 4 + t] = np.v[t];
         }
-        gbar(0);
-        if (q == 0 && valid && w == W_NONE) st_release(plan.ver + (size_t)j * f.nx + i, (unsigned)s + 1u);
+#ifdef BAND_SERIAL_PREFETCH
+        asm volatile("barrier.cta.arrive 6, %0;" ::"r"(THREADS) : "memory");
+#endif
       } else {
+#ifdef BAND_SERIAL_PREFETCH
+        asm volatile("barrier.cta.sync 6, %0;" ::"r"(THREADS) : "memory");
+#endif
         const int wi = warp - 4;
+        // publish step d-1: its write-back happened before the last CTA
+        // barrier, so this release orders it (fence cumulativity) and the
+        // update's critical path carries no memory fence
+        if (wi == 0 && d > dfirst) {
+          const int cl = b.cell(c, d - 1);
+          if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
+        }
         if (d + 1 <= dlast)
           band_load<M, 4>(f, plan.ver, b, d + 2, 0, 33, (unsigned)s, smem + LY::V_X * VEC, SPV, smem + LY::PX, wi,
                           12, err, plan.poll_ns);
@@ -328,12 +361,17 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       if (tr) s_tr[6] += gtimer() - s_tr[3];
       if (s_stop) return;
     }
+    if (warp == 4) {  // publish the last step
+      const int cl = b.cell(c, dlast);
+      if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
+    }
     if (tr) {
       unsigned long long* o = plan.trace + (size_t)task * 16;
       // [loop start, end, steps | s << 20 | k << 28, sums from step start
       //  to: copies, faces, update, prefetch, step end]
       o[0] = s_tr[1];
       o[1] = gtimer();
+      s_tr[10] = clock64() - s_tr[10];  // SM cycles over the loop (effective clock)
       o[2] = (unsigned long long)(dlast - dfirst + 1) | ((unsigned long long)s << 20) | ((unsigned long long)k << 28);
       o[3] = s_tr[4];
       o[4] = s_tr[5];

@@ -111,9 +111,19 @@ __device__ __forceinline__ void project2(int g, int q, double* a, const P4& af, 
     double ca[M + 1], cb[M + 1];
     coeffs<M>(af, at, d, ca);
     coeffs<M>(bf, bt, d, cb);
-    if (act_a && act_b) pass_two<M>(q, d, a, ca, true, b, cb, true);
-    else if (act_a) pass<M>(q, d, a, ca);
-    else if (act_b) pass<M>(q, d, b, cb);
+    if (act_a || act_b) pass_two<M>(q, d, a, ca, act_a, b, cb, act_b);
+    gbar(g);
+  }
+}
+
+// single-vector projection (one pass body per call site)
+template <int M>
+__device__ __forceinline__ void project1(int g, int q, double* a, const P4& af, const P4& at, bool act_a) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double ca[M + 1];
+    coeffs<M>(af, at, d, ca);
+    if (act_a) pass<M>(q, d, a, ca);
     gbar(g);
   }
 }
@@ -395,17 +405,21 @@ __device__ __forceinline__ void flux_q(int branch, bool high, double un, double 
 }
 
 __device__ __forceinline__ unsigned long long gtimer0() {
+#ifdef TRACE_CLOCK
+  return (unsigned long long)clock64() * 1000ull / 1965ull;
+#else
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+#endif
 }
 
 // Phases 1-4 of one face group on states already staged in L / U
 // (face_flux, flux.cpp:77-132, and the back projection of spatial.cpp:118-125).
 // branch: B_HALF (interior face, lp / rp the face states' bases) or B_WALL
 // (L = the cell state in basis cp); invalid lanes pass B_NONE.
-template <int M, int AXIS>
-__device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, bool high, int branch, int fail,
+template <int M>
+__device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, int axis, bool high, int branch, int fail,
                                          const P4& lp, const P4& rp, const P4& cp, double* L, double* U,
                                          double* F, unsigned long long* stamp) {
   P4 fp{};
@@ -413,9 +427,13 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, bool h
   P4 wb{};
   double rs = 1.0;
   if (branch == B_WALL) {
-    // constant indices only: a runtime index would copy ctx to local memory
-    wb.v[AXIS == 0 ? 1 : 0] = high ? ctx.wall_speed[2 * AXIS + 1] : ctx.wall_speed[2 * AXIS];
-    wb.v[3] = high ? ctx.wall_theta[2 * AXIS + 1] : ctx.wall_theta[2 * AXIS];
+    // selects only: a runtime index would copy ctx / wb to local memory
+    const double ws = axis == 0 ? (high ? ctx.wall_speed[1] : ctx.wall_speed[0])
+                                : (high ? ctx.wall_speed[3] : ctx.wall_speed[2]);
+    wb.v[0] = axis == 0 ? 0.0 : ws;
+    wb.v[1] = axis == 0 ? ws : 0.0;
+    wb.v[3] = axis == 0 ? (high ? ctx.wall_theta[1] : ctx.wall_theta[0])
+                        : (high ? ctx.wall_theta[3] : ctx.wall_theta[2]);
     if (!(wb.v[3] > 0.0)) {
       fail = W_PROJ_SPREAD;
       branch = B_NONE;
@@ -423,7 +441,8 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, bool h
       rs = sqrt(wb.v[3]);
     }
   } else if (branch == B_HALF) {
-    const double ul = rep_u32(L, lp, AXIS), ur = rep_u32(U, rp, AXIS);
+    const double ul = (axis == 0 ? lp.v[0] : lp.v[1]) + L[(1 + axis) * SPV] / L[0];
+    const double ur = (axis == 0 ? rp.v[0] : rp.v[1]) + U[(1 + axis) * SPV] / U[0];
     const double cl = ctx.c_bound * sqrt(rep_theta32(L, lp));
     const double cr = ctx.c_bound * sqrt(rep_theta32(U, rp));
     const double lminus = tc::smin(ul - cl, ur - cr);
@@ -450,10 +469,16 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, bool h
   // ---- phase 3: flux in the face basis into F (per-partition K columns)
   double kin0[M + 1];
   {
-    const double un = branch == B_WALL ? 0.0 : fp.v[AXIS];
-#define SP_FQ(Q) flux_q<M, AXIS, Q>(branch, high, un, rs, fp, L, U, F, kin0)
-    SP_DISPATCH(q, SP_FQ)
+    const double un = branch == B_WALL ? 0.0 : (axis == 0 ? fp.v[0] : fp.v[1]);
+    if (axis == 0) {
+#define SP_FQ(Q) flux_q<M, 0, Q>(branch, high, un, rs, fp, L, U, F, kin0)
+      SP_DISPATCH(q, SP_FQ)
 #undef SP_FQ
+    } else {
+#define SP_FQ(Q) flux_q<M, 1, Q>(branch, high, un, rs, fp, L, U, F, kin0)
+      SP_DISPATCH(q, SP_FQ)
+#undef SP_FQ
+    }
   }
   gbar(g);
   if (stamp) stamp[2] = gtimer0();
@@ -468,7 +493,7 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, bool h
     } else {
 #pragma unroll
       for (int p = 1; p <= M; ++p) {
-        const int k = AXIS == 0 ? flat3(p, 0, 0) : flat3(0, p, 0);
+        const int k = axis == 0 ? flat3(p, 0, 0) : flat3(0, p, 0);
         F[k * SPV] = fma(wall_rho, kin0[p], F[k * SPV]);
       }
       F[0] = 0.0;
@@ -477,7 +502,7 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, bool h
   gbar(g);
   // ---- phase 4: flux back into the cell basis (in F)
   const P4 from = branch == B_WALL ? wb : fp;
-  project2<M>(g, q, F, from, cp, branch != B_NONE, U, cp, cp, false);
+  project1<M>(g, q, F, from, cp, branch != B_NONE);
   return fail;
 }
 
@@ -634,7 +659,7 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
   }
   gbar(g);
   if (stamp) stamp[0] = gtimer0();
-  fail = face_core<M, AXIS>(ctx, g, q, high, branch, fail, lp, rp, cp, L, U, F, stamp);
+  fail = face_core<M>(ctx, g, q, AXIS, high, branch, fail, lp, rp, cp, L, U, F, stamp);
   *cp_out = cp;
   return fail;
 }
@@ -646,7 +671,12 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
 template <int M>
 __device__ __forceinline__ int update_split(const DevField& f, const DevField* rhs, const DevCtx& ctx,
                                             int q, bool valid, int i, int j, double* base, double* bad,
-                                            P4 cp, double dxi, double dyj, P4* new_p = nullptr) {
+                                            P4 cp, double dxi, double dyj, P4* new_p = nullptr,
+                                            unsigned long long* dbg = nullptr) {
+  // dbg (one thread, debug): [0] step start; accumulators [8] scalars,
+  // [9] assembled, [10] normalize iterations, [11] normalized, [12] written
+#define US_STAMP(slot) \
+  if (dbg) dbg[slot] += gtimer0() - dbg[0]
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, VEC = Layout<M>::VEC;
   const int c = threadIdx.x & 31;
   double* S = base + 12 * VEC + c;      // SB (staged in the face phase)
@@ -683,7 +713,8 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
       }
     }
   }
-  if (rhs) project2<M>(0, q, RH, rp, cp, valid && fail == W_NONE, V, cp, cp, false);
+  US_STAMP(8);
+  if (rhs) project1<M>(0, q, RH, rp, cp, valid && fail == W_NONE);
   const bool ok0 = valid && fail == W_NONE;
   if (ok0) {
     const double idx = 1.0 / dxi, idy = 1.0 / dyj;
@@ -695,6 +726,7 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
 #undef SP_AS
   }
   gbar(0);
+  US_STAMP(9);
   // apply_update with the dt/2 retry; grad_normalize loop uniform per group
   bool done = !ok0;
   bool good = false;
@@ -742,7 +774,8 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
         }
       }
       if (!gbar_or(0, need)) break;
-      project2<M>(0, q, V, prm, to, need, D, cp, cp, false);
+      if (dbg) dbg[10] += 1;
+      project1<M>(0, q, V, prm, to, need);
       if (need) prm = to;
     }
     if (!done) {
@@ -762,6 +795,7 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
     }
     if (!gbar_or(0, !done)) break;
   }
+  US_STAMP(11);
   // coalesced write-back: warp q stores cells 8q..8q+7, lane = coefficient
   {
     const int lane = threadIdx.x & 31;
@@ -781,12 +815,19 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
 #pragma unroll
       for (int h = 0; h < (N + 31) / 32; ++h) {
         const int k = lane + 32 * h;
+#ifdef WB_PLAIN
+        if (k < N) dst[k] = Vb[k * SPV + cc];
+#else
         if (k < N) __stcg(dst + k, Vb[k * SPV + cc]);
+#endif
       }
     }
-    __threadfence();
+    // no fence here: the caller publishes the cells with st.release after a
+    // CTA barrier, which orders every thread's write-back (cumulativity)
   }
   if (new_p) *new_p = prm;
+  US_STAMP(12);
+#undef US_STAMP
   return (valid && !good && fail == W_NONE) ? W_DT_HALVING : fail;
 }
 
@@ -807,9 +848,13 @@ struct SegPlan32 {
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
+#ifdef TRACE_CLOCK  // SM cycle counter scaled to ns at 1965 MHz (per-SM, not global)
+  return (unsigned long long)clock64() * 1000ull / 1965ull;
+#else
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+#endif
 }
 
 template <int M, int ORDER>

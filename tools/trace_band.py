@@ -35,8 +35,13 @@ print(f"tasks {got}  span {(t[:, 1].max() - t0) / 1e3:.1f} us")
 print("per-step means, us from step start: copies %.2f  faces %.2f  update %.2f  prefetch %.2f  end %.2f;"
       "  loop time/step %.2f" % tuple([np.sum(t[:, q]) / S / 1e3 for q in (3, 4, 5, 6, 7)]
                                       + [np.sum(t[:, 1] - t[:, 0]) / S / 1e3]))
+print("update detail, us from step start: scalars %.2f  assembled %.2f  normalized %.2f  written %.2f;"
+      "  normalize iterations/step %.2f" % tuple([np.sum(t[:, q]) / S / 1e3 for q in (11, 12, 14, 15)]
+                                                 + [np.sum(t[:, 13]) / S]))
 print("face detail (group 0), us from step start: projected %.2f  flux %.2f" % tuple(
     np.sum(t[:, q]) / S / 1e3 for q in (8, 9)))
+print("effective SM clock over the step loops: %.0f MHz (median over tasks)" % np.median(
+    t[:, 10] / np.maximum(t[:, 1] - t[:, 0], 1) * 1e3))
 print(" task  s   k  loop(us)  end(us)  steps  us/step")
 rows = [int(x) for x in os.environ.get('ROWS', '').split(',') if x] or (list(range(0, min(4, got))) + list(range(nb - 2, nb + 2)) + list(range(got - 3, got)))
 for r in rows:
