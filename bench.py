@@ -101,6 +101,17 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def band_traffic(nx):
+    """DRAM bytes (read + write) per launch of the band sweep measured by ncu at
+    this grid size (profiles/r1_band_traffic.json, from tools/profile.sh), or None."""
+    path = os.path.join(ROOT, "profiles", "r1_band_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d["bytes_per_launch"] if d.get("nx") == nx else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def fp64_peak():
     p = os.path.join(ROOT, "profiles", "fp64_peak.json")
     if os.path.exists(p):
@@ -309,10 +320,13 @@ def ours(a):
     sweep_med = statistics.median(sweep_ms)
     achieved = FLOPS_PER_UPDATE_C5 * updates / (sweep_med * 1e-3) / 1e12
     roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": None, "kernel": "k_sweep_persistent<5>",
+            "frac": achieved / peak, "traffic": band_traffic(nx), "kernel": "sp::k5_band<5,32>",
             "flops_per_update": FLOPS_PER_UPDATE_C5, "peak_source": peak_src,
             "kernel_ms": sweep_med,
-            "note": "FP64 CUDA cores (no tensor-core path); hbm bytes/update >= 960, AI ~17 flop/B"}
+            "note": ("FP64 CUDA cores (no tensor-core path); hbm bytes/update >= 960, AI ~17 flop/B. "
+                     "Exact Gauss-Seidel order: the sweep DAG has ~2.5 (nx+ny) dependent levels per "
+                     "FS iteration, so the kernel is bound by the latency of one 32-cell diagonal "
+                     "step (kernel_ms / levels), not by FP64 or HBM throughput (DESIGN.md sec. 5)")}
 
     cpu = None
     if not a.no_cpu and rank == 0 and world == 1:

@@ -57,15 +57,16 @@ struct BandLayout {
   static constexpr int PV = PX + 132;  // params of V [32][4]
   static constexpr int HALO = PV + 128;  // band k-1 new state [N] + params [4]
   static constexpr int HALOP = HALO + N;
-  static constexpr size_t bytes = (size_t)(HALOP + 4) * sizeof(double);
+  static constexpr int PRE = HALOP + 4;  // 2 blocks [PRE_N][32] of precomputed update scalars
+  static constexpr size_t bytes = (size_t)(PRE + 2 * PRE_N * 32) * sizeof(double);
 };
 
 struct BandGeo {
-  int nx, ny, k;
+  int nx, ny, k, bw;
   bool i_up, j_up;
   // rotated cell (ir = 32k + slot, jr = dd - ir) -> flat index, or -1
   __device__ __forceinline__ int cell(int slot, int dd) const {
-    const int ir = 32 * k + slot, jr = dd - ir;
+    const int ir = bw * k + slot, jr = dd - ir;
     if (ir < 0 || ir >= nx || jr < 0 || jr >= ny) return -1;
     const int i = i_up ? ir : nx - 1 - ir, j = j_up ? jr : ny - 1 - jr;
     return j * nx + i;
@@ -147,15 +148,81 @@ __device__ __forceinline__ void band_load(const DevField& fld, const unsigned* v
   }
 }
 
+// Update scalars (cell_scalars) of the cells of diagonal dd, whose states
+// and bases are in OLD1 / PO, into a PRE block: one step ahead of the cell
+// update, by a warp that is otherwise idle, so that pow / sqrt / divisions
+// are off the critical path.
+template <int M, int BW>
+__device__ __forceinline__ void band_pre(const DevField& f, const DevCtx& ctx, const BandGeo& b, int dd,
+                                         const double* OLD1, const double* PO, double* pre) {
+  const int c = threadIdx.x & 31;
+  const int ir = BW * b.k + c, jr = dd - ir;
+  const bool valid = c < BW && ir < f.nx && jr >= 0 && jr < f.ny;
+  double dt = 0.0, nu = 0.0, qv[3] = {0.0, 0.0, 0.0}, idx = 1.0, idy = 1.0;
+  int fail = W_NONE;
+  if (valid) {
+    const int i = b.i_up ? ir : f.nx - 1 - ir, j = b.j_up ? jr : f.ny - 1 - jr;
+    const double dxi = f.dx[i], dyj = f.dy[j];
+    P4 cp;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cp.v[t] = PO[c * 4 + t];
+    fail = cell_scalars(ctx, OLD1 + c, cp, dxi, dyj, &dt, &nu, qv);
+    idx = 1.0 / dxi;
+    idy = 1.0 / dyj;
+  }
+  pre[PRE_DT * 32 + c] = dt;
+  pre[PRE_NU * 32 + c] = nu;
+  pre[PRE_Q0 * 32 + c] = qv[0];
+  pre[PRE_Q0 * 32 + 32 + c] = qv[1];
+  pre[PRE_Q0 * 32 + 64 + c] = qv[2];
+  pre[PRE_FAIL * 32 + c] = (double)fail;
+  pre[PRE_IDX * 32 + c] = idx;
+  pre[PRE_IDY * 32 + c] = idy;
+}
+
+// Write-back of the cells of diagonal dd updated by the previous step: new
+// states V (group 1's L, interleaved) and bases PV, for the lanes whose
+// update succeeded (ok).  Warp w of 16 stores cells 2w and 2w+1, lane =
+// coefficient (coalesced).  Runs at the start of the next step on all warps,
+// so the update's critical path ends with its last projection pass.
 template <int M>
+__device__ __forceinline__ void band_writeback(const DevField& f, const BandGeo& b, int dd, const double* V,
+                                               const double* PV, const int* ok, int warp) {
+  constexpr int N = Gen<M>::N, NP = (N + 3) & ~3;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int cc = 2 * warp + t;
+    const int cl = ok[cc] ? b.cell(cc, dd) : -1;
+    if (cl < 0) continue;
+    double* dst = f.c + (size_t)cl * NP;
+    double r[(N + 31) / 32];
+#pragma unroll
+    for (int h = 0; h < (N + 31) / 32; ++h) {
+      const int k = lane + 32 * h;
+      r[h] = k < N ? V[k * SPV + cc] : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < (N + 31) / 32; ++h) {
+      const int k = lane + 32 * h;
+      if (k < N) __stcg(dst + k, r[h]);
+    }
+    if (lane < 4) __stcg(f.p + (size_t)cl * 4 + lane, PV[cc * 4 + lane]);
+  }
+}
+
+template <int M, int BW>
 __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, DevErr* err, BandPlan plan) {
+  static_assert(BW == 16 || BW == 32, "band width: 16 or 32 columns");
+  constexpr int NS = BW + 1;  // slots of the old-state vectors (one column of band k+1)
   extern __shared__ __align__(128) double smem[];
   __shared__ int s_task, s_stop;
+  __shared__ int s_ok[32];  // per-lane success of the last cell update (write-back pending)
   __shared__ unsigned long long s_tr[16];  // debug trace accumulators (thread 0)
   __shared__ unsigned long long s_ph[4];   // debug: face phase stamps of group 0
   using LY = BandLayout<M>;
   constexpr int N = LY::N, VEC = LY::VEC;
-  constexpr int NE = 33 * N;                         // elements of one 33-slot vector
+  constexpr int NE = NS * N;                         // elements of one NS-slot vector
   constexpr int EPT = (NE + THREADS - 1) / THREADS;  // per thread in the copy phase
   const int tid = threadIdx.x;
   const int warp = tid >> 5, g = warp / P, q = warp % P, c = tid & 31;
@@ -174,10 +241,11 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     b.nx = f.nx;
     b.ny = f.ny;
     b.k = k;
+    b.bw = BW;
     b.i_up = dir == 0 || dir == 3;  // kSweepDirs (single_level.cpp:116-117)
     b.j_up = dir == 0 || dir == 1;
-    const int ir = 32 * k + c;
-    const int dfirst = 32 * k, dlast = min(32 * k + 31, f.nx - 1) + f.ny - 1;
+    const int ir = BW * k + c;
+    const int dfirst = BW * k, dlast = min(BW * k + BW - 1, f.nx - 1) + f.ny - 1;
     const bool tr = plan.trace && 2 * task + 1 < plan.trace_cap && tid == 0;
     if (tr) {
       s_tr[0] = gtimer();
@@ -187,9 +255,9 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     // first two diagonals and band k-1's halo cell, then every warp loads
     // OLD1 <- old(dfirst), X <- old(dfirst+1), HALO <- band k-1 at dfirst-1
     if (warp == 0) {
-      for (int e = c; e < 67; e += 32) {
-        const int cl = e < 66 ? b.cell(e % 33, dfirst + e / 33) : (k > 0 ? b.cell(-1, dfirst - 1) : -1);
-        const unsigned need = e < 66 ? (unsigned)s : (unsigned)s + 1u;
+      for (int e = c; e < 2 * NS + 1; e += 32) {
+        const int cl = e < 2 * NS ? b.cell(e % NS, dfirst + e / NS) : (k > 0 ? b.cell(-1, dfirst - 1) : -1);
+        const unsigned need = e < 2 * NS ? (unsigned)s : (unsigned)s + 1u;
         if (cl >= 0 && need) {
           long long polls = 0;
           while (ld_relaxed(plan.ver + cl) < need) {
@@ -205,17 +273,22 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       }
     }
     __syncthreads();
-    band_load<M, 4>(f, plan.ver, b, dfirst, 0, 33, 0u, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp, 16, err, 0);
-    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, 33, 0u, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err, 0);
+    band_load<M, 4>(f, plan.ver, b, dfirst, 0, NS, 0u, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp, 16, err, 0);
+    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, NS, 0u, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err, 0);
     if (k > 0 && warp == 15)
       band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, 0u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1, err, 0);
     __syncthreads();
+    if (warp == 4)
+      band_pre<M, BW>(f, ctx, b, dfirst, smem + LY::V_OLD1 * VEC, smem + LY::PO, smem + LY::PRE + (dfirst & 1) * PRE_N * 32);
+    __syncthreads();  // (A) of the first step overwrites OLD1 / PO
     if (tr) {
       s_tr[1] = gtimer();
       s_tr[10] = clock64();
     }
     for (int d = dfirst; d <= dlast; ++d) {
       if (tr) s_tr[3] = gtimer();
+      // write-back of step d-1 (V is read here before (A) overwrites it)
+      if (d > dfirst) band_writeback<M>(f, b, d - 1, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
       // ---- (A) stage the step's face states.  Sources: OLD1 (own old
       // states), X (old states of diagonal d+1), V (= L of group 1: new
       // states of d-1) and HALO.  Every destination except group 1's L is
@@ -233,15 +306,15 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
           const int e = tid + r * THREADS;
           hold[r] = 0.0;
           if (e < NE) {
-            const int kk = e / 33, sl = e - kk * 33;
+            const int kk = e / NS, sl = e - kk * NS;
             const int o = kk * SPV + sl;
             const double x = X[o];
-            if (sl < 32) {
+            if (sl < BW) {
               const double self = OLD1[o];
               const double xu = sl ? Vv[o - 1] : HALO[kk];
               const double yu = Vv[o];
               const double xd = X[o + 1];
-              const int irs = 32 * k + sl, jrs = d - irs;
+              const int irs = BW * k + sl, jrs = d - irs;
               const bool sxu = irs >= 1, sxd = irs + 1 < f.nx, syu = jrs >= 1, syd = jrs + 1 < f.ny;
               smem[LY::V_S * VEC + o] = self;
               // face group gg: the neighbour is the lower cell of a low face
@@ -264,7 +337,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       }
       // this lane's parameters and geometry
       const int jr = d - ir;
-      const bool valid = ir < f.nx && jr >= 0 && jr < f.ny;
+      const bool valid = c < BW && ir < f.nx && jr >= 0 && jr < f.ny;
       const int i = valid ? (b.i_up ? ir : f.nx - 1 - ir) : 0;
       const int j = valid ? (b.j_up ? jr : f.ny - 1 - jr) : 0;
       P4 cp, lp, rp;
@@ -287,21 +360,17 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         lp = low ? nb : cp;
         rp = low ? cp : nb;
       }
-      double dxi = 1.0, dyj = 1.0;
-      if (valid && g == 0) {
-        dxi = f.dx[i];
-        dyj = f.dy[j];
-      }
+      const double dxi = 1.0, dyj = 1.0;  // the update takes 1/dx, 1/dy and dt from PRE
       __syncthreads();
 #pragma unroll
       for (int r = 0; r < EPT; ++r) {
         const int e = tid + r * THREADS;
         if (e < NE) {
-          const int kk = e / 33, sl = e - kk * 33;
-          if (sl < 32) smem[3 * VEC + kk * SPV + sl] = hold[r];
+          const int kk = e / NS, sl = e - kk * NS;
+          if (sl < BW) smem[3 * VEC + kk * SPV + sl] = hold[r];
         }
       }
-      if (tid < 132) smem[LY::PO + tid] = smem[LY::PX + tid];
+      if (tid < 4 * NS) smem[LY::PO + tid] = smem[LY::PX + tid];
       __syncthreads();
       if (tr) s_tr[4] += gtimer() - s_tr[3];
       // ---- (B) face fluxes (face_flux / wall_flux, back into the cell basis)
@@ -324,10 +393,10 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         double bad = 0.0;
         P4 np = cp;
         const int w = update_split<M>(f, nullptr, ctx, q, valid, i, j, smem, &bad, cp, dxi, dyj, &np,
-                                      tr ? s_tr + 3 : nullptr);
+                                      tr ? s_tr + 3 : nullptr, smem + LY::PRE + (d & 1) * PRE_N * 32 + c, s_ok);
         if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
         if (tr) s_tr[7] += gtimer() - s_tr[3];
-        if (q == 0) {
+        if (q == 0 && c < BW) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) smem[LY::PV + c * 4 + t] = np.v[t];
         }
@@ -342,13 +411,16 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         // publish step d-1: its write-back happened before the last CTA
         // barrier, so this release orders it (fence cumulativity) and the
         // update's critical path carries no memory fence
-        if (wi == 0 && d > dfirst) {
+        if (wi == 0 && d > dfirst && c < BW) {
           const int cl = b.cell(c, d - 1);
           if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
         }
         if (d + 1 <= dlast)
-          band_load<M, 4>(f, plan.ver, b, d + 2, 0, 33, (unsigned)s, smem + LY::V_X * VEC, SPV, smem + LY::PX, wi,
+          band_load<M, 4>(f, plan.ver, b, d + 2, 0, NS, (unsigned)s, smem + LY::V_X * VEC, SPV, smem + LY::PX, wi,
                           12, err, plan.poll_ns);
+        if (wi == 0 && d + 1 <= dlast)  // OLD1 / PO hold diagonal d+1 since (A)
+          band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
+                          smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         if (k > 0 && wi == 11 && d + 1 <= dlast)
           band_load<M, 1>(f, plan.ver, b, d, -1, 1, (unsigned)s + 1u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1,
                           err, plan.poll_ns);
@@ -361,7 +433,9 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       if (tr) s_tr[6] += gtimer() - s_tr[3];
       if (s_stop) return;
     }
-    if (warp == 4) {  // publish the last step
+    band_writeback<M>(f, b, dlast, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
+    __syncthreads();
+    if (warp == 4 && c < BW) {  // publish the last step
       const int cl = b.cell(c, dlast);
       if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
     }

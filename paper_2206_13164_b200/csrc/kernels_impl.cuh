@@ -458,13 +458,14 @@ struct Launch {
           if (ctx.order == 1 && !rhs && band_sweep_enabled()) {
             static bool battr = false;
             if (!battr) {
-              set_smem(sp::k5_band<M>, sp::BandLayout<M>::bytes);
+              set_smem(sp::k5_band<M, 32>, sp::BandLayout<M>::bytes);
               battr = true;
             }
+            const int bw = 32;  // columns per band task (16 measured no faster per step: latency-bound)
             sp::BandPlan bp;
             band_scratch(f, &bp.ver, &bp.next);
             bp.nsweeps = 4 * iters;
-            bp.nbands = (f->nx + 31) / 32;
+            bp.nbands = (f->nx + bw - 1) / bw;
             bp.dirbits = 0;
             for (int s = 0; s < 16; ++s) {
               bp.dirs[s] = order[s & 3];
@@ -474,9 +475,9 @@ struct Launch {
             poll_tuning(&sw, &bp.poll_ns);
             bp.exp = sw;
             bp.trace = trace_buffer(&bp.trace_cap);
-            int nb = tc_sweep_blocks((const void*)sp::k5_band<M>, sp::BandLayout<M>::bytes, sp::THREADS);
+            int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
             if (nb > bp.nsweeps * bp.nbands) nb = bp.nsweeps * bp.nbands;
-            sp::k5_band<M><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp);
+            sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp);
             momg_rt::count_launch(1);
             return;
           }

@@ -490,6 +490,7 @@ bool band_sweep_enabled() {
 }
 void set_band_mode(int m) { g_band = m; }
 
+
 static int g_split = -1;
 bool split_sweep_enabled() {
   if (g_split < 0) {
@@ -745,9 +746,14 @@ static int upload(momg_field* f, const double* coeffs, const double* params, mom
   ENSURE();
   if (!f || !coeffs || !params) return arg_error(err, "momg_field_upload: null argument");
   const size_t cells = (size_t)f->nx * f->ny;
-  cudaError_t e = cudaMemcpy2DAsync(f->c, f->NP * sizeof(double), coeffs, f->N * sizeof(double),
-                                    f->N * sizeof(double), cells, cudaMemcpyHostToDevice,
-                                    momg_rt::stream());
+  // unpadded records (N % 4 == 0, e.g. M = 5): one linear copy (a pitched copy
+  // of millions of short rows runs far below the PCIe rate)
+  cudaError_t e = f->NP == f->N
+                      ? cudaMemcpyAsync(f->c, coeffs, cells * f->N * sizeof(double), cudaMemcpyHostToDevice,
+                                        momg_rt::stream())
+                      : cudaMemcpy2DAsync(f->c, f->NP * sizeof(double), coeffs, f->N * sizeof(double),
+                                          f->N * sizeof(double), cells, cudaMemcpyHostToDevice,
+                                          momg_rt::stream());
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(f->p, params, cells * 4 * sizeof(double), cudaMemcpyHostToDevice,
                         momg_rt::stream());
@@ -762,8 +768,11 @@ static int download(const momg_field* f, double* coeffs, double* params, momg_er
   const size_t cells = (size_t)f->nx * f->ny;
   cudaError_t e = cudaSuccess;
   if (coeffs)
-    e = cudaMemcpy2DAsync(coeffs, f->N * sizeof(double), f->c, f->NP * sizeof(double),
-                          f->N * sizeof(double), cells, cudaMemcpyDeviceToHost, momg_rt::stream());
+    e = f->NP == f->N ? cudaMemcpyAsync(coeffs, f->c, cells * f->N * sizeof(double), cudaMemcpyDeviceToHost,
+                                        momg_rt::stream())
+                      : cudaMemcpy2DAsync(coeffs, f->N * sizeof(double), f->c, f->NP * sizeof(double),
+                                          f->N * sizeof(double), cells, cudaMemcpyDeviceToHost,
+                                          momg_rt::stream());
   if (e == cudaSuccess && params)
     e = cudaMemcpyAsync(params, f->p, cells * 4 * sizeof(double), cudaMemcpyDeviceToHost,
                         momg_rt::stream());

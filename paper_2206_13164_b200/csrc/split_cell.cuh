@@ -349,11 +349,12 @@ __device__ __forceinline__ void part_store(int q, const double* v, double* dst) 
 // half / full flux.  Partition 0 also returns row 0 of the incoming-side
 // wall kernel for the wall closure.
 template <int M, int AXIS, int Q>
-__device__ __forceinline__ void flux_q(int branch, bool high, double un, double rs, const P4& fp, const double* L,
-                                       const double* U, double* F, double (&kin0)[M + 1]) {
+__device__ __forceinline__ void flux_q(int branch, bool high, double un, double rs, const tc::HalfBase& hb,
+                                       const P4& fp, const double* L, const double* U, double* F,
+                                       double (&kin0)[M + 1]) {
   if (branch == B_HALF || branch == B_WALL) {
     double Ku[M + 1][M + 1], Kl[M + 1][M + 1];
-    tc::half_kernels<M>(un, rs, Ku, Kl);
+    tc::half_kernels_b<M>(un, rs, hb, Ku, Kl);
     if (branch == B_HALF) {
       if constexpr (AXIS == 0) {
         if constexpr (Q == 0) Split<M, P>::half_sum0_0(L, U, Ku, Kl, F);
@@ -470,12 +471,14 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, int ax
   double kin0[M + 1];
   {
     const double un = branch == B_WALL ? 0.0 : (axis == 0 ? fp.v[0] : fp.v[1]);
+    // one erfc / exp per face, shared by the 8 partition x axis flux bodies
+    const tc::HalfBase hb = tc::half_base(un, rs);
     if (axis == 0) {
-#define SP_FQ(Q) flux_q<M, 0, Q>(branch, high, un, rs, fp, L, U, F, kin0)
+#define SP_FQ(Q) flux_q<M, 0, Q>(branch, high, un, rs, hb, fp, L, U, F, kin0)
       SP_DISPATCH(q, SP_FQ)
 #undef SP_FQ
     } else {
-#define SP_FQ(Q) flux_q<M, 1, Q>(branch, high, un, rs, fp, L, U, F, kin0)
+#define SP_FQ(Q) flux_q<M, 1, Q>(branch, high, un, rs, hb, fp, L, U, F, kin0)
       SP_DISPATCH(q, SP_FQ)
 #undef SP_FQ
     }
@@ -668,11 +671,35 @@ __device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, 
 // sweep_cell (single_level.cpp:103-111): local dt, residual assembly
 // (spatial.cpp:127-132), rhs projection (update_delta :64-70), the update and
 // grad_normalize with the dt/2 retry (apply_update :44-62); face group 0.
+// Per-cell scalars of the update from the cell's current state S (lane's
+// column, stride SPV) and basis cp: local_dt (single_level.cpp:18-29), the
+// collision frequency (collision.hpp:36-44) and, for Shakhov, the heat flux
+// of extract_macro (moment_rep.hpp:134-144).  Returns the failure kind.
+__device__ __forceinline__ int cell_scalars(const DevCtx& ctx, const double* S, const P4& cp, double dxi,
+                                            double dyj, double* dt, double* nu, double* qv) {
+  if (!(cp.v[3] > 0.0)) return W_DT_THETA;
+  const double cc = ctx.cfl_c_bound * sqrt(cp.v[3]);
+  *dt = ctx.cfl / ((fabs(cp.v[0]) + cc) / dxi + (fabs(cp.v[1]) + cc) / dyj);
+  const double rho = S[0];
+  if (!(rho > 0.0)) return W_MACRO_RHO;
+  if (ctx.collision == 1) return W_ES_UNSUPPORTED;
+  *nu = ctx.nu_coef * rho * pow(cp.v[3], ctx.nu_exp);
+  if (ctx.collision == 2) {
+    qv[0] = 2.0 * S[flat3(3, 0, 0) * SPV] + S[flat3(3, 0, 0) * SPV] + S[flat3(1, 2, 0) * SPV] + S[flat3(1, 0, 2) * SPV];
+    qv[1] = 2.0 * S[flat3(0, 3, 0) * SPV] + S[flat3(2, 1, 0) * SPV] + S[flat3(0, 3, 0) * SPV] + S[flat3(0, 1, 2) * SPV];
+    qv[2] = 2.0 * S[flat3(0, 0, 3) * SPV] + S[flat3(2, 0, 1) * SPV] + S[flat3(0, 2, 1) * SPV] + S[flat3(0, 0, 3) * SPV];
+  }
+  return W_NONE;
+}
+// layout of a precomputed scalar block: value t of lane c at pre[t * 32 + c]
+enum : int { PRE_DT = 0, PRE_NU = 1, PRE_Q0 = 2, PRE_FAIL = 5, PRE_IDX = 6, PRE_IDY = 7, PRE_N = 8 };
+
 template <int M>
 __device__ __forceinline__ int update_split(const DevField& f, const DevField* rhs, const DevCtx& ctx,
                                             int q, bool valid, int i, int j, double* base, double* bad,
                                             P4 cp, double dxi, double dyj, P4* new_p = nullptr,
-                                            unsigned long long* dbg = nullptr) {
+                                            unsigned long long* dbg = nullptr, const double* pre = nullptr,
+                                            int* ok_out = nullptr) {
   // dbg (one thread, debug): [0] step start; accumulators [8] scalars,
   // [9] assembled, [10] normalize iterations, [11] normalized, [12] written
 #define US_STAMP(slot) \
@@ -695,29 +722,22 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
   int fail = W_NONE;
   double dt = 0.0, nu = 0.0, qv[3] = {0.0, 0.0, 0.0};
   if (valid) {
-    if (!(cp.v[3] > 0.0)) {
-      fail = W_DT_THETA;
+    if (pre) {  // computed ahead from the same cell state (band sweep)
+      dt = pre[PRE_DT * 32];
+      nu = pre[PRE_NU * 32];
+      qv[0] = pre[PRE_Q0 * 32];
+      qv[1] = pre[PRE_Q0 * 32 + 32];
+      qv[2] = pre[PRE_Q0 * 32 + 64];
+      fail = (int)pre[PRE_FAIL * 32];
     } else {
-      const double cc = ctx.cfl_c_bound * sqrt(cp.v[3]);
-      dt = ctx.cfl / ((fabs(cp.v[0]) + cc) / dxi + (fabs(cp.v[1]) + cc) / dyj);
-      const double rho = S[0];
-      if (!(rho > 0.0)) fail = W_MACRO_RHO;
-      else if (ctx.collision == 1) fail = W_ES_UNSUPPORTED;
-      else {
-        nu = ctx.nu_coef * rho * pow(cp.v[3], ctx.nu_exp);
-        if (ctx.collision == 2) {
-          qv[0] = 2.0 * S[flat3(3, 0, 0) * SPV] + S[flat3(3, 0, 0) * SPV] + S[flat3(1, 2, 0) * SPV] + S[flat3(1, 0, 2) * SPV];
-          qv[1] = 2.0 * S[flat3(0, 3, 0) * SPV] + S[flat3(2, 1, 0) * SPV] + S[flat3(0, 3, 0) * SPV] + S[flat3(0, 1, 2) * SPV];
-          qv[2] = 2.0 * S[flat3(0, 0, 3) * SPV] + S[flat3(2, 0, 1) * SPV] + S[flat3(0, 2, 1) * SPV] + S[flat3(0, 0, 3) * SPV];
-        }
-      }
+      fail = cell_scalars(ctx, S, cp, dxi, dyj, &dt, &nu, qv);
     }
   }
   US_STAMP(8);
   if (rhs) project1<M>(0, q, RH, rp, cp, valid && fail == W_NONE);
   const bool ok0 = valid && fail == W_NONE;
   if (ok0) {
-    const double idx = 1.0 / dxi, idy = 1.0 / dyj;
+    const double idx = pre ? pre[PRE_IDX * 32] : 1.0 / dxi, idy = pre ? pre[PRE_IDY * 32] : 1.0 / dyj;
     const int shk = ctx.collision == 2;
     const double shw = ctx.shakhov_w;
     const bool hr = rhs != nullptr;
@@ -797,7 +817,10 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
   }
   US_STAMP(11);
   // coalesced write-back: warp q stores cells 8q..8q+7, lane = coefficient
-  {
+  // (ok_out: the caller stores V later; only the per-cell flag is returned)
+  if (ok_out) {
+    if (q == 0) ok_out[threadIdx.x & 31] = valid && fail == W_NONE && good;
+  } else {
     const int lane = threadIdx.x & 31;
     const bool ok = valid && fail == W_NONE && good;
     if (ok && q == 0) {

@@ -163,12 +163,32 @@ __device__ __forceinline__ int grad_normalize(double* v, P4& prm, double* bad) {
 //   Ku[m][p] = rs^(p-m)/p! (u_n P+(m,p) + rs P+(m+1,p) + rs m P+(m-1,p)),
 //   Kl[m][p] = same with P- = m! delta - P+.
 // The pairing table follows the reference recurrence column by column.
+// The transcendental part of the base row (one erfc, one exp per face):
+// a = -u_n / rs, g = e^{-a^2/2}/sqrt(2 pi), e0 = erfc(a/sqrt 2)/2.
+struct HalfBase {
+  double a, g, e0;
+};
+__device__ __forceinline__ HalfBase half_base(double un, double rs) {
+  HalfBase h;
+  h.a = -un / rs;
+  h.g = exp(-h.a * h.a * 0.5) * 0.3989422804014327;
+  h.e0 = 0.5 * erfc(h.a * 0.7071067811865476);
+  return h;
+}
+template <int M>
+__device__ __forceinline__ void half_kernels_b(double un, double rs, const HalfBase& hb,
+                                               double (&Ku)[M + 1][M + 1], double (&Kl)[M + 1][M + 1]);
 template <int M>
 __device__ __forceinline__ void half_kernels(double un, double rs, double (&Ku)[M + 1][M + 1],
                                              double (&Kl)[M + 1][M + 1]) {
+  half_kernels_b<M>(un, rs, half_base(un, rs), Ku, Kl);
+}
+template <int M>
+__device__ __forceinline__ void half_kernels_b(double un, double rs, const HalfBase& hb,
+                                               double (&Ku)[M + 1][M + 1], double (&Kl)[M + 1][M + 1]) {
   constexpr int P = M + 1;
-  const double a = -un / rs;
-  const double g = exp(-a * a * 0.5) * 0.3989422804014327;  // e^{-a^2/2}/sqrt(2 pi)
+  const double a = hb.a;
+  const double g = hb.g;
   double he[P + 1];
   he[0] = 1.0;
   he[1] = a;
@@ -180,7 +200,7 @@ __device__ __forceinline__ void half_kernels(double un, double rs, double (&Ku)[
 #pragma unroll
   for (int p = 0; p <= M; ++p) {
     double col[P + 1];
-    col[0] = p == 0 ? 0.5 * erfc(a * 0.7071067811865476) : he[p - 1] * g;
+    col[0] = p == 0 ? hb.e0 : he[p - 1] * g;
 #pragma unroll
     for (int m = 0; m + 1 <= P; ++m) {
       const double t = he[m] * he[p] * g;

@@ -20,7 +20,8 @@ c, p = c5_field(n, n, M, seed=1)
 f = momg.CellField.from_host(g, M, c, p)
 momg.fast_sweep_step(f, None, ctx)
 L = momg.lib()
-nb = (n + 31) // 32
+bw = 32
+nb = (n + bw - 1) // bw
 cap = 4 * nb
 L.momg_debug_trace(C.c_longlong(2 * cap))
 momg.fast_sweep_step(f, None, ctx)
