@@ -100,6 +100,8 @@ __device__ __forceinline__ void band_load(const DevField& fld, const unsigned* v
     if (slot < s0 + ns) my_cell = b.cell(slot, dd);
   }
   if (need && my_cell >= 0) {
+    // relaxed polling, one acquire once satisfied (an acquire per poll
+    // measured slower: the spinning warps slow the SM's memory pipeline)
     const unsigned* a = ver + my_cell;
     long long polls = 0;
     while (ld_relaxed(a) < need) {
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
   __shared__ int s_ok[32];  // per-lane success of the last cell update (write-back pending)
   __shared__ unsigned long long s_tr[16];  // debug trace accumulators (thread 0)
   __shared__ unsigned long long s_ph[4];   // debug: face phase stamps of group 0
+  __shared__ unsigned long long s_warr[16];  // debug: per-warp arrival at the end-of-step barrier
   using LY = BandLayout<M>;
   constexpr int N = LY::N, VEC = LY::VEC;
   constexpr int NE = NS * N;                         // elements of one NS-slot vector
@@ -246,11 +249,12 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     b.j_up = dir == 0 || dir == 1;
     const int ir = BW * k + c;
     const int dfirst = BW * k, dlast = min(BW * k + BW - 1, f.nx - 1) + f.ny - 1;
-    const bool tr = plan.trace && 2 * task + 1 < plan.trace_cap && tid == 0;
+    const bool tr = plan.trace && 4 * task + 3 < plan.trace_cap && tid == 0;
     if (tr) {
       s_tr[0] = gtimer();
       for (int t = 2; t < 16; ++t) s_tr[t] = 0;
     }
+    if (plan.trace && 4 * task + 3 < plan.trace_cap && c == 0) s_warr[warp] = 0;
     // prologue: warp 0 alone waits (with back-off) for the cells of the
     // first two diagonals and band k-1's halo cell, then every warp loads
     // OLD1 <- old(dfirst), X <- old(dfirst+1), HALO <- band k-1 at dfirst-1
@@ -387,8 +391,8 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         s_tr[9] += s_ph[2] - s_tr[3];
       }
       // ---- (C) face group 0: cell update (update_split); groups 1-3:
-      // publish the previous step's cells, prefetch old(d+2) and band k-1's
-      // new cell for the next step
+      // publish the previous step's cells, band k-1's new cell and old(d+2)
+      // for the next step, update scalars of d+1
       if (g == 0) {
         double bad = 0.0;
         P4 np = cp;
@@ -400,14 +404,9 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
 #pragma unroll
           for (int t = 0; t < 4; ++t) smem[LY::PV + c * 4 + t] = np.v[t];
         }
-#ifdef BAND_SERIAL_PREFETCH
-        asm volatile("barrier.cta.arrive 6, %0;" ::"r"(THREADS) : "memory");
-#endif
       } else {
-#ifdef BAND_SERIAL_PREFETCH
-        asm volatile("barrier.cta.sync 6, %0;" ::"r"(THREADS) : "memory");
-#endif
         const int wi = warp - 4;
+        const int stop_now = tid == 128 ? band_stop(err) : 0;  // issued early, consumed last
         // publish step d-1: its write-back happened before the last CTA
         // barrier, so this release orders it (fence cumulativity) and the
         // update's critical path carries no memory fence
@@ -421,14 +420,16 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         if (wi == 0 && d + 1 <= dlast)  // OLD1 / PO hold diagonal d+1 since (A)
           band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
                           smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
+        // band k-1's new cell last: by then it is (nearly always) published
         if (k > 0 && wi == 11 && d + 1 <= dlast)
           band_load<M, 1>(f, plan.ver, b, d, -1, 1, (unsigned)s + 1u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1,
                           err, plan.poll_ns);
         if (tid == 128) {
-          s_stop = band_stop(err);
-          if (plan.trace && 2 * task + 1 < plan.trace_cap) s_tr[2] += gtimer() - s_tr[3];
+          s_stop = stop_now;
+          if (plan.trace && 4 * task + 3 < plan.trace_cap) s_tr[2] += gtimer() - s_tr[3];
         }
       }
+      if (plan.trace && 4 * task + 3 < plan.trace_cap && c == 0) s_warr[warp] += gtimer() - s_tr[3];
       __syncthreads();
       if (tr) s_tr[6] += gtimer() - s_tr[3];
       if (s_stop) return;
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
     }
     if (tr) {
-      unsigned long long* o = plan.trace + (size_t)task * 16;
+      unsigned long long* o = plan.trace + (size_t)task * 32;
       // [loop start, end, steps | s << 20 | k << 28, sums from step start
       //  to: copies, faces, update, prefetch, step end]
       o[0] = s_tr[1];
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       o[6] = s_tr[2];
       o[7] = s_tr[6];
       for (int t = 8; t < 16; ++t) o[t] = s_tr[t];
+      for (int t = 0; t < 16; ++t) o[16 + t] = s_warr[t];
     }
   }
 }

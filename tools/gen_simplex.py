@@ -27,6 +27,7 @@ import os
 import sys
 
 ORDERS = [3, 4, 5, 6, 7, 8]
+SPLIT_PASS_CHAINS = False
 
 
 def simplex(M):
@@ -178,7 +179,7 @@ def lpt(costs, P):
     return parts
 
 
-def emit_split(M, P):
+def emit_split(M, P, full=True):
     idx = simplex(M)
     pos = {a: k for k, a in enumerate(idx)}
     N = len(idx)
@@ -210,9 +211,17 @@ def emit_split(M, P):
                         out.append(f"    const double {tag}{t}_{j} = {vec}[{k} * SPV];")
                 for t, ks in enumerate(mine):
                     for j in range(len(ks) - 1, 0, -1):
+                        # (splitting into odd / even chains measured slower)
                         expr = f"{tag}{t}_{j}"
+                        odd = None
                         for n in range(1, j + 1):
-                            expr = f"fma({cn}[{n}], {tag}{t}_{j - n}, {expr})"
+                            if SPLIT_PASS_CHAINS and j >= 3 and n % 2 == 1:
+                                odd = (f"{cn}[{n}] * {tag}{t}_{j - n}" if odd is None
+                                       else f"fma({cn}[{n}], {tag}{t}_{j - n}, {odd})")
+                            else:
+                                expr = f"fma({cn}[{n}], {tag}{t}_{j - n}, {expr})"
+                        if odd is not None:
+                            expr = f"{expr} + {odd}"
                         st = f"{vec}[{ks[j]} * SPV] = {expr};"
                         out.append(f"    if ({guard}) {st}" if guard else f"    {st}")
                 return out
@@ -227,6 +236,11 @@ def emit_split(M, P):
             nla = sum(len(ks) for ks in mine)
             L.extend(la[:nla] + lb[:nla] + la[nla:] + lb[nla:])
             w("  }")
+    if not full:  # pass-only variant (the band sweep's 16-warp normalisation)
+        bounds = [round(q * N / P) for q in range(P + 1)]
+        w(f"  static constexpr int KLO[{P + 1}] = {{" + ", ".join(map(str, bounds)) + "};")
+        w("};")
+        return "\n".join(L)
     # half sums split by the normal index p
     for a in range(2):
         tans = {}
@@ -256,11 +270,17 @@ def emit_split(M, P):
                         if not single:
                             w(f"      const double r{m} = Rv[{k} * SPV];")
                     for p in ps:
-                        expr = None
+                        # two independent FMA chains (upper: L rows, lower: R
+                        # rows; single: even / odd m) halve the dependency depth
+                        eu = el = None
                         for m in range(len(ks)):
-                            expr = f"l{m} * Ku[{m}][{p}]" if expr is None else f"fma(l{m}, Ku[{m}][{p}], {expr})"
+                            if single and m % 2 == 1:
+                                el = f"l{m} * Ku[{m}][{p}]" if el is None else f"fma(l{m}, Ku[{m}][{p}], {el})"
+                            else:
+                                eu = f"l{m} * Ku[{m}][{p}]" if eu is None else f"fma(l{m}, Ku[{m}][{p}], {eu})"
                             if not single:
-                                expr = f"fma(r{m}, Kl[{m}][{p}], {expr})"
+                                el = f"r{m} * Kl[{m}][{p}]" if el is None else f"fma(r{m}, Kl[{m}][{p}], {el})"
+                        expr = eu if el is None else f"{eu} + {el}"
                         w(f"      o[{ks[p]} * SPV] = {expr};")
                     w("    }")
                 w("  }")

@@ -23,10 +23,10 @@ L = momg.lib()
 bw = 32
 nb = (n + bw - 1) // bw
 cap = 4 * nb
-L.momg_debug_trace(C.c_longlong(2 * cap))
+L.momg_debug_trace(C.c_longlong(4 * cap))
 momg.fast_sweep_step(f, None, ctx)
-buf = np.zeros((cap, 16), dtype=np.uint64)
-got = L.momg_debug_trace_read(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_longlong(2 * cap)) // 2
+buf = np.zeros((cap, 32), dtype=np.uint64)
+got = L.momg_debug_trace_read(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_longlong(4 * cap)) // 4
 t = buf[:got].astype(np.float64)
 steps = (buf[:got, 2] & 0xfffff).astype(np.float64)
 sk = [(int(v >> 20) & 0xff, int(v >> 28)) for v in buf[:got, 2]]
@@ -41,6 +41,8 @@ print("update detail, us from step start: scalars %.2f  assembled %.2f  normaliz
                                                  + [np.sum(t[:, 13]) / S]))
 print("face detail (group 0), us from step start: projected %.2f  flux %.2f" % tuple(
     np.sum(t[:, q]) / S / 1e3 for q in (8, 9)))
+print("per-warp arrival at the end-of-step barrier, us from step start:",
+      " ".join("%.2f" % (np.sum(t[:, 16 + w]) / S / 1e3) for w in range(16)))
 print("effective SM clock over the step loops: %.0f MHz (median over tasks)" % np.median(
     t[:, 10] / np.maximum(t[:, 1] - t[:, 0], 1) * 1e3))
 print(" task  s   k  loop(us)  end(us)  steps  us/step")
