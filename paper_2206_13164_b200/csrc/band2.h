@@ -1,0 +1,29 @@
+// Host-side interface of the second-order / right-hand-side band sweep
+// (band2_sweep.cuh, compiled in band2_m<M>.cu with its own vector stride).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "types.h"
+
+namespace momg_gpu {
+namespace sp {
+struct Band2Plan {
+  unsigned* ver;   // per-cell sweep counters (zeroed per launch)
+  unsigned* next;  // task counter (zeroed per launch)
+  int nsweeps;     // <= 16
+  int nbands;      // ceil(nx / 16)
+  unsigned dirbits;
+  int order;       // 1 | 2
+  int has_rhs;
+  int poll_ns;
+};
+}  // namespace sp
+struct DevCtx;
+void band2_launch_m3(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err,
+                     const sp::Band2Plan& plan, cudaStream_t st);
+void band2_launch_m4(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err,
+                     const sp::Band2Plan& plan, cudaStream_t st);
+void band2_launch_m5(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err,
+                     const sp::Band2Plan& plan, cudaStream_t st);
+}  // namespace momg_gpu

@@ -22,6 +22,7 @@
 #include "kernels_v3.cuh"
 #include "split_cell.cuh"
 #include "band_sweep.cuh"
+#include "band2.h"
 
 namespace momg_gpu {
 
@@ -357,6 +358,7 @@ unsigned long long* trace_buffer(long long* cap);
 void poll_tuning(int* split_wait, int* poll_ns);
 void band_scratch(momg_field* f, unsigned** ver, unsigned** next);
 bool band_sweep_enabled();
+bool band2_enabled();
 void set_band_mode(int m);
 const uint32_t* split_schedule(momg_field* f, int nsweeps, const int* dirs, int radius, int seg);
 
@@ -478,6 +480,24 @@ struct Launch {
             int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
             if (nb > bp.nsweeps * bp.nbands) nb = bp.nsweeps * bp.nbands;
             sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp);
+            momg_rt::count_launch(1);
+            return;
+          }
+          if (band_sweep_enabled() && band2_enabled()) {
+            // second order and/or an FAS rhs: the 16-column band sweep
+            sp::Band2Plan bp;
+            band_scratch(f, &bp.ver, &bp.next);
+            bp.nsweeps = 4 * iters;
+            bp.nbands = (f->nx + 15) / 16;
+            bp.dirbits = 0;
+            for (int s = 0; s < 16; ++s) bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
+            bp.order = ctx.order;
+            bp.has_rhs = rhs != nullptr;
+            int sw = 0;
+            poll_tuning(&sw, &bp.poll_ns);
+            if constexpr (M == 3) band2_launch_m3(fd, rd, c, err, bp, momg_rt::stream());
+            else if constexpr (M == 4) band2_launch_m4(fd, rd, c, err, bp, momg_rt::stream());
+            else band2_launch_m5(fd, rd, c, err, bp, momg_rt::stream());
             momg_rt::count_launch(1);
             return;
           }

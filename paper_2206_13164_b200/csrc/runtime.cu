@@ -490,6 +490,17 @@ bool band_sweep_enabled() {
 }
 void set_band_mode(int m) { g_band = m; }
 
+// second-order / rhs sweeps on the 16-column band kernel (MOMG_BAND2=0: the
+// wavefront-item kernel k4_sweep)
+bool band2_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("MOMG_BAND2");
+    on = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  return on == 1;
+}
+
 
 static int g_split = -1;
 bool split_sweep_enabled() {
