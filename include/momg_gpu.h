@@ -115,6 +115,16 @@ int momg_field_upload(momg_field* f, const double* coeffs, const double* params,
 int momg_field_download(const momg_field* f, double* coeffs, double* params, momg_err* err);
 int momg_field_upload_async(momg_field* f, const double* coeffs, const double* params, momg_err* err);
 int momg_field_download_async(const momg_field* f, double* coeffs, double* params, momg_err* err);
+/* Overlapped transfers for streaming many solves through double-buffered
+ * fields: the upload runs on the library's H2D copy stream once the field's
+ * previous overlapped download has finished, and every kernel enqueued after
+ * the call waits for it; the download runs on the D2H copy stream after the
+ * kernels enqueued before the call.  Host buffers should be pinned.  Finish
+ * with momg_synchronize (which also waits for both copy streams). */
+int momg_field_upload_overlapped(momg_field* f, const double* coeffs, const double* params, momg_err* err);
+int momg_field_download_overlapped(momg_field* f, double* coeffs, double* params, momg_err* err);
+/* make later work on the library stream wait for every overlapped transfer enqueued so far */
+int momg_copy_barrier(momg_err* err);
 int momg_field_copy(momg_field* dst, const momg_field* src, momg_err* err);   /* CellField copy (multigrid.cpp:188) */
 int momg_field_fill_maxwellian(momg_field* f, double rho, const double u[3], double theta,
                                momg_err* err);                               /* uniform_field (grid.hpp:79-85) */

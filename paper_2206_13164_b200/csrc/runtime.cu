@@ -650,6 +650,10 @@ momg_field* field_new(int M, int nx, int ny, double Lx, double Ly, const double*
 void field_free(momg_field* f) {
   if (!f) return;
   cudaStreamSynchronize(momg_rt::stream());
+  if (f->ev_free) {
+    cudaEventSynchronize(f->ev_free);
+    cudaEventDestroy(f->ev_free);
+  }
   cudaFree(f->c);
   cudaFree(f->p);
   cudaFree(f->dgrid);
@@ -701,9 +705,11 @@ int momg_set_stream(void* s) {
   return MOMG_OK;
 }
 void* momg_get_stream(void) { return (void*)momg_rt::stream(); }
+void copy_streams_sync();
 int momg_synchronize(momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  copy_streams_sync();
   return momg_rt::sync_check(err);
 }
 const char* momg_version(void) { return "momg_gpu 0.1 (sm_100a, FP64)"; }
@@ -801,6 +807,73 @@ int momg_field_upload_async(momg_field* f, const double* c, const double* p, mom
 }
 int momg_field_download_async(const momg_field* f, double* c, double* p, momg_err* err) {
   return download(f, c, p, err, false);
+}
+// ---- overlapped transfers (double-buffered streaming of solves)
+static cudaStream_t g_h2d = nullptr, g_d2h = nullptr;
+static bool copy_streams() {
+  if (!g_h2d && cudaStreamCreateWithFlags(&g_h2d, cudaStreamNonBlocking) != cudaSuccess) return false;
+  if (!g_d2h && cudaStreamCreateWithFlags(&g_d2h, cudaStreamNonBlocking) != cudaSuccess) return false;
+  return true;
+}
+void copy_streams_sync() {
+  if (g_h2d) cudaStreamSynchronize(g_h2d);
+  if (g_d2h) cudaStreamSynchronize(g_d2h);
+}
+int momg_field_upload_overlapped(momg_field* f, const double* coeffs, const double* params, momg_err* err) {
+  CLEAR_ERR();
+  ENSURE();
+  if (!f || !coeffs || !params) return arg_error(err, "momg_field_upload_overlapped: null argument");
+  if (!copy_streams()) return momg_rt::cuda_check(cudaErrorUnknown, err, "momg_field_upload_overlapped");
+  const size_t cells = (size_t)f->nx * f->ny;
+  cudaError_t e = cudaSuccess;
+  if (f->ev_free) e = cudaStreamWaitEvent(g_h2d, f->ev_free, 0);
+  if (e == cudaSuccess)
+    e = f->NP == f->N ? cudaMemcpyAsync(f->c, coeffs, cells * f->N * sizeof(double), cudaMemcpyHostToDevice, g_h2d)
+                      : cudaMemcpy2DAsync(f->c, f->NP * sizeof(double), coeffs, f->N * sizeof(double),
+                                          f->N * sizeof(double), cells, cudaMemcpyHostToDevice, g_h2d);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(f->p, params, cells * 4 * sizeof(double), cudaMemcpyHostToDevice, g_h2d);
+  cudaEvent_t ev = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, g_h2d);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(momg_rt::stream(), ev, 0);
+  if (ev) cudaEventDestroy(ev);  // released once complete
+  return momg_rt::cuda_check(e, err, "momg_field_upload_overlapped");
+}
+int momg_field_download_overlapped(momg_field* f, double* coeffs, double* params, momg_err* err) {
+  CLEAR_ERR();
+  ENSURE();
+  if (!f || !coeffs || !params) return arg_error(err, "momg_field_download_overlapped: null argument");
+  if (!copy_streams()) return momg_rt::cuda_check(cudaErrorUnknown, err, "momg_field_download_overlapped");
+  const size_t cells = (size_t)f->nx * f->ny;
+  cudaEvent_t ev = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, momg_rt::stream());
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(g_d2h, ev, 0);
+  if (ev) cudaEventDestroy(ev);
+  if (e == cudaSuccess)
+    e = f->NP == f->N ? cudaMemcpyAsync(coeffs, f->c, cells * f->N * sizeof(double), cudaMemcpyDeviceToHost, g_d2h)
+                      : cudaMemcpy2DAsync(coeffs, f->N * sizeof(double), f->c, f->NP * sizeof(double),
+                                          f->N * sizeof(double), cells, cudaMemcpyDeviceToHost, g_d2h);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(params, f->p, cells * 4 * sizeof(double), cudaMemcpyDeviceToHost, g_d2h);
+  if (e == cudaSuccess && !f->ev_free) e = cudaEventCreateWithFlags(&f->ev_free, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(f->ev_free, g_d2h);
+  return momg_rt::cuda_check(e, err, "momg_field_download_overlapped");
+}
+int momg_copy_barrier(momg_err* err) {
+  CLEAR_ERR();
+  ENSURE();
+  cudaError_t e = cudaSuccess;
+  for (cudaStream_t st : {g_h2d, g_d2h}) {
+    if (!st || e != cudaSuccess) continue;
+    cudaEvent_t ev = nullptr;
+    e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(momg_rt::stream(), ev, 0);
+    if (ev) cudaEventDestroy(ev);
+  }
+  return momg_rt::cuda_check(e, err, "momg_copy_barrier");
 }
 int momg_field_copy(momg_field* dst, const momg_field* src, momg_err* err) {
   CLEAR_ERR();

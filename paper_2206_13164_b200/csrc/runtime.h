@@ -23,6 +23,7 @@ struct momg_field {
   int* seg_plan = nullptr;          // thread-granular sweep: diag_lo | seg_start (lazy)
   int* seg_plan32 = nullptr;        // split sweep (32-cell segments)
   struct Schedule* schedule = nullptr;  // split sweep: cached dependency-level item order
+  cudaEvent_t ev_free = nullptr;        // overlapped transfers: last download of this field done
   DevField dev() const {
     DevField d;
     d.nx = nx;

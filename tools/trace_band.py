@@ -52,3 +52,8 @@ for r in rows:
         s, k = sk[r]
         print(f"{r:5d} {s:2d} {k:3d} {(t[r,0]-t0)/1e3:8.1f} {(t[r,1]-t0)/1e3:8.1f} "
               f"{int(steps[r]):6d} {(t[r,1]-t[r,0])/steps[r]/1e3:8.2f}")
+for r in [int(x) for x in os.environ.get('WROWS', '0,1,2,64').split(',') if x]:
+    if 0 <= r < got:
+        print(f"task {r}: per-warp arrival (us from step start):",
+              " ".join("%.2f" % (t[r, 16 + w] / steps[r] / 1e3) for w in range(16)),
+              "| faces %.2f update %.2f end %.2f" % tuple(t[r, q] / steps[r] / 1e3 for q in (4, 5, 7)))
