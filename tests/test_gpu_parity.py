@@ -109,20 +109,26 @@ def test_sweep_order_and_rhs(order, sweep_mode):
     assert np.max(np.abs(gp - wp)) < TOL
 
 
-# Band tasks (first order, M <= 5): grids wider than one 32-column band, so
-# the inter-band halo, partial bands and every sweep direction are exercised.
+# Band tasks (M <= 5): grids wider than one band (32 columns at first order
+# without rhs, k5_band; 16 columns at second order or with an FAS rhs,
+# k6_band), so the inter-band halos (radius 2 at second order), partial bands
+# and every sweep direction are exercised.
 BAND_CASES = [
-    # (M, model, nx, ny, sweep order, with rhs)
-    (5, BGK, 70, 37, (0, 1, 2, 3), False),
-    (3, SHAKHOV, 33, 5, (2, 0, 3, 1), True),
-    (4, BGK, 64, 40, (1, 1, 3, 3), True),
-    (5, SHAKHOV, 40, 66, (3, 2, 1, 0), True),
+    # (M, model, nx, ny, sweep order, with rhs, space order)
+    (5, BGK, 70, 37, (0, 1, 2, 3), False, 1),
+    (3, SHAKHOV, 33, 5, (2, 0, 3, 1), True, 1),
+    (4, BGK, 64, 40, (1, 1, 3, 3), True, 1),
+    (5, SHAKHOV, 40, 66, (3, 2, 1, 0), True, 1),
+    (5, BGK, 50, 35, (0, 1, 2, 3), False, 2),
+    (3, SHAKHOV, 34, 20, (2, 0, 3, 1), True, 2),
+    (4, BGK, 40, 33, (1, 1, 3, 3), True, 2),
+    (5, SHAKHOV, 17, 48, (3, 2, 1, 0), True, 2),
 ]
 
 
-@pytest.mark.parametrize("M,model,nx,ny,order,with_rhs", BAND_CASES)
-def test_band_sweep_parity(M, model, nx, ny, order, with_rhs):
-    g, octx, c, p = _setup(M, 1, model, nx, ny, True)
+@pytest.mark.parametrize("M,model,nx,ny,order,with_rhs,space", BAND_CASES)
+def test_band_sweep_parity(M, model, nx, ny, order, with_rhs, space):
+    g, octx, c, p = _setup(M, space, model, nx, ny, True)
     rhs_h = None
     if with_rhs:
         rc = c * 1e-3
@@ -137,6 +143,34 @@ def test_band_sweep_parity(M, model, nx, ny, order, with_rhs):
         gc, gp = f.download()
         assert rel_field(gc, wc) < TOL, f"iteration {it}"
         assert np.max(np.abs(gp - wp)) < TOL
+
+
+def test_overlapped_transfers_double_buffer():
+    """momg_field_{upload,download}_overlapped: a double-buffered stream of
+    solves gives the same results as the synchronous path."""
+    g, octx, c, p = _setup(5, 1, BGK, 40, 24, True)
+    ctx = mctx(octx)
+    f0 = momg.CellField.from_host(mgrid(g), 5, c, p)
+    momg.fast_sweep_step(f0, None, ctx)
+    want_c, want_p = f0.download()
+    L, C = momg.lib(), momg.C
+    flds = [momg.CellField(mgrid(g), 5), momg.CellField(mgrid(g), 5)]
+    hc, hp = np.ascontiguousarray(c), np.ascontiguousarray(p)
+    outs = [(np.zeros_like(c), np.zeros_like(p)) for _ in range(3)]
+    e = momg._Err()
+    assert L.momg_field_upload_overlapped(flds[0].handle, momg._dp(hc), momg._dp(hp), C.byref(e)) == 0
+    for s_ in range(3):
+        cur, nxt = flds[s_ % 2], flds[(s_ + 1) % 2]
+        momg.fast_sweep_step(cur, None, ctx)
+        if s_ < 2:
+            assert L.momg_field_upload_overlapped(nxt.handle, momg._dp(hc), momg._dp(hp), C.byref(e)) == 0
+        oc, op = outs[s_]
+        assert L.momg_field_download_overlapped(cur.handle, momg._dp(oc), momg._dp(op), C.byref(e)) == 0
+    assert L.momg_copy_barrier(C.byref(e)) == 0
+    assert L.momg_synchronize(C.byref(e)) == 0
+    for oc, op in outs:
+        np.testing.assert_array_equal(oc, want_c)
+        np.testing.assert_array_equal(op, want_p)
 
 
 @pytest.mark.parametrize("M", [3, 5, 6, 8])
