@@ -28,6 +28,18 @@ __global__ void k_axpy(double* dst, const double* src, size_t n, const DevErr* e
     dst[q] += src[q];
 }
 
+// defect without a right-hand side (multigrid.cpp:183-185: defect = -res):
+// a flat, coalesced pass over the coefficient records (padding copied) and
+// the basis parameters (copied: the defect keeps the residual's basis)
+__global__ void k_negate(const double* __restrict__ src_c, const double* __restrict__ src_p, double* dst_c,
+                         double* dst_p, size_t ncoef, int N, int NP, size_t nparam, const DevErr* err) {
+  if (err_set(err)) return;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < ncoef; q += stride)
+    dst_c[q] = (int)(q % NP) < N ? -src_c[q] : src_c[q];
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < nparam; q += stride) dst_p[q] = src_p[q];
+}
+
 __global__ void k_scale(double* c, size_t n, const double* factor_dev, const DevErr* err) {
   if (err_set(err)) return;
   const double f = *factor_dev;
@@ -559,6 +571,13 @@ void op_fas(momg_field* fine, const momg_field* before, const momg_field* after)
   ops_for(fine->M)->fas(fine, before, after);
 }
 void op_defect(const momg_field* res, const momg_field* rhs, momg_field* out) {
+  if (!rhs) {
+    const size_t cells = (size_t)res->nx * res->ny;
+    k_negate<<<148 * 8, 256, 0, momg_rt::stream()>>>(res->c, res->p, out->c, out->p, cells * res->NP, res->N,
+                                                     res->NP, cells * 4, momg_rt::err_dev());
+    momg_rt::count_launch(1);
+    return;
+  }
   ops_for(res->M)->defect(res, rhs, out);
 }
 void op_axpy(momg_field* dst, const momg_field* src) {
