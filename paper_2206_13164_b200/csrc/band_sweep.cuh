@@ -43,6 +43,7 @@ struct BandPlan {
   int exp;  // experiment flags (debug timing only; results invalid when set)
   unsigned long long* trace;  // optional per-task [8] stamps (debug)
   long long trace_cap;
+  int nchunks, clen;  // residual mode: diagonal chunks per band and their length
 };
 
 template <int M>
@@ -213,8 +214,14 @@ __device__ __forceinline__ void band_writeback(const DevField& f, const BandGeo&
   }
 }
 
-template <int M, int BW>
-__global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, DevErr* err, BandPlan plan) {
+// RES = true: the residual (spatial.cpp:135-159) with the same staging and
+// face machinery.  Every neighbour is an old state, nothing waits on a
+// counter, tasks are (band, chunk of diagonals) so all SMs have work, and the
+// previous diagonal's states (V) are the old ones, copied there by group 0
+// after it assembles R = Q - sum of the face fluxes, which it stores to `out`.
+template <int M, int BW, bool RES = false>
+__global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, DevErr* err, BandPlan plan,
+                                                      DevField out) {
   static_assert(BW == 16 || BW == 32, "band width: 16 or 32 columns");
   constexpr int NS = BW + 1;  // slots of the old-state vectors (one column of band k+1)
   extern __shared__ __align__(128) double smem[];
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
   constexpr int EPT = (NE + THREADS - 1) / THREADS;  // per thread in the copy phase
   const int tid = threadIdx.x;
   const int warp = tid >> 5, g = warp / P, q = warp % P, c = tid & 31;
-  const int ntasks = plan.nsweeps * plan.nbands;
+  const int ntasks = RES ? plan.nchunks * plan.nbands : plan.nsweeps * plan.nbands;
   for (;;) {
     if (tid == 0) {
       s_task = (int)atomicAdd(plan.next, 1u);
@@ -238,8 +245,8 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     __syncthreads();
     const int task = s_task;
     if (task >= ntasks || s_stop) return;
-    const int s = task / plan.nbands, k = task % plan.nbands;
-    const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
+    const int s = RES ? 0 : task / plan.nbands, k = task % plan.nbands;
+    const int dir = RES ? 0 : (int)((plan.dirbits >> (2 * s)) & 3u);
     BandGeo b;
     b.nx = f.nx;
     b.ny = f.ny;
@@ -248,7 +255,15 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     b.i_up = dir == 0 || dir == 3;  // kSweepDirs (single_level.cpp:116-117)
     b.j_up = dir == 0 || dir == 1;
     const int ir = BW * k + c;
-    const int dfirst = BW * k, dlast = min(BW * k + BW - 1, f.nx - 1) + f.ny - 1;
+    int dfirst = BW * k, dlast = min(BW * k + BW - 1, f.nx - 1) + f.ny - 1;
+    if (RES) {
+      dfirst += (task / plan.nbands) * plan.clen;
+      dlast = min(dlast, dfirst + plan.clen - 1);
+      if (dfirst > dlast) {  // empty chunk of a partial band
+        __syncthreads();
+        continue;
+      }
+    }
     const bool tr = plan.trace && 4 * task + 3 < plan.trace_cap && tid == 0;
     if (tr) {
       s_tr[0] = gtimer();
@@ -258,7 +273,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     // prologue: warp 0 alone waits (with back-off) for the cells of the
     // first two diagonals and band k-1's halo cell, then every warp loads
     // OLD1 <- old(dfirst), X <- old(dfirst+1), HALO <- band k-1 at dfirst-1
-    if (warp == 0) {
+    if (!RES && warp == 0) {
       for (int e = c; e < 2 * NS + 1; e += 32) {
         const int cl = e < 2 * NS ? b.cell(e % NS, dfirst + e / NS) : (k > 0 ? b.cell(-1, dfirst - 1) : -1);
         const unsigned need = e < 2 * NS ? (unsigned)s : (unsigned)s + 1u;
@@ -281,6 +296,9 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, NS, 0u, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err, 0);
     if (k > 0 && warp == 15)
       band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, 0u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1, err, 0);
+    if (RES)  // a chunk may start mid-band: its upstream states are old(dfirst-1)
+      band_load<M, 2>(f, plan.ver, b, dfirst - 1, 0, BW, 0u, smem + LY::V_V * VEC, SPV, smem + LY::PV, warp, 16,
+                      err, 0);
     __syncthreads();
     if (warp == 4)
       band_pre<M, BW>(f, ctx, b, dfirst, smem + LY::V_OLD1 * VEC, smem + LY::PO, smem + LY::PRE + (dfirst & 1) * PRE_N * 32);
@@ -292,7 +310,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     for (int d = dfirst; d <= dlast; ++d) {
       if (tr) s_tr[3] = gtimer();
       // write-back of step d-1 (V is read here before (A) overwrites it)
-      if (d > dfirst) band_writeback<M>(f, b, d - 1, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
+      if (!RES && d > dfirst) band_writeback<M>(f, b, d - 1, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
       // ---- (A) stage the step's face states.  Sources: OLD1 (own old
       // states), X (old states of diagonal d+1), V (= L of group 1: new
       // states of d-1) and HALO.  Every destination except group 1's L is
@@ -393,7 +411,56 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       // ---- (C) face group 0: cell update (update_split); groups 1-3:
       // publish the previous step's cells, band k-1's new cell and old(d+2)
       // for the next step, update scalars of d+1
-      if (g == 0) {
+      if (RES && g == 0) {
+        // residual: R = Q - sum of the face fluxes into D (group 1's U) and
+        // V <- S (old states of d for the next diagonal's upstream faces)
+        const double* pre = smem + LY::PRE + (d & 1) * PRE_N * 32 + c;
+        const int w = valid ? (int)pre[PRE_FAIL * 32] : W_NONE;
+        double* S = smem + LY::V_S * VEC + c;
+        double* V = smem + LY::V_V * VEC + c;
+        double* D = V + VEC;
+        if (valid && w == W_NONE) {
+          const double qv[3] = {pre[PRE_Q0 * 32], pre[PRE_Q0 * 32 + 32], pre[PRE_Q0 * 32 + 64]};
+#define RS_AS(Q)                                                                                              \
+  Part<M, Q>::assemble(S, nullptr, smem + 2 * VEC + c, smem + 5 * VEC + c, smem + 8 * VEC + c,                \
+                       smem + 11 * VEC + c, pre[PRE_NU * 32], ctx.collision == 2, ctx.shakhov_w, qv,         \
+                       pre[PRE_IDX * 32], pre[PRE_IDY * 32], 0.0, false, D, V)
+          SP_DISPATCH(q, RS_AS)
+#undef RS_AS
+        }
+        if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, 0.0);
+#define RS_CP(Q) Part<M, Q>::copy(S, V)
+        SP_DISPATCH(q, RS_CP)
+#undef RS_CP
+        gbar(0);
+        {  // coalesced store of R: warp q stores cells 8q..8q+7, lane = coefficient
+          constexpr int NP = (N + 3) & ~3;
+          const bool ok = valid && w == W_NONE;
+          const size_t cell = (size_t)j * f.nx + i;
+          if (ok && q == 0) {
+            __stcg(reinterpret_cast<double2*>(out.p + cell * 4), make_double2(cp.v[0], cp.v[1]));
+            __stcg(reinterpret_cast<double2*>(out.p + cell * 4) + 1, make_double2(cp.v[2], cp.v[3]));
+          }
+          const double* Db = D - c;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int cc = 8 * q + t;
+            const int okc = __shfl_sync(0xffffffffu, ok ? 1 : 0, cc);
+            const long long bc = __shfl_sync(0xffffffffu, (long long)cell, cc);
+            if (!okc) continue;
+            double* dst = out.c + (size_t)bc * NP;
+#pragma unroll
+            for (int h = 0; h < (N + 31) / 32; ++h) {
+              const int kq = c + 32 * h;
+              if (kq < N) __stcg(dst + kq, Db[kq * SPV + cc]);
+            }
+          }
+        }
+        if (q == 0 && c < BW) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) smem[LY::PV + c * 4 + t] = cp.v[t];
+        }
+      } else if (g == 0) {
         double bad = 0.0;
         P4 np = cp;
         const int w = update_split<M>(f, nullptr, ctx, q, valid, i, j, smem, &bad, cp, dxi, dyj, &np,
@@ -410,7 +477,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         // publish step d-1: its write-back happened before the last CTA
         // barrier, so this release orders it (fence cumulativity) and the
         // update's critical path carries no memory fence
-        if (wi == 0 && d > dfirst && c < BW) {
+        if (!RES && wi == 0 && d > dfirst && c < BW) {
           const int cl = b.cell(c, d - 1);
           if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
         }
@@ -422,8 +489,8 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
                           smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         // band k-1's new cell last: by then it is (nearly always) published
         if (k > 0 && wi == 11 && d + 1 <= dlast)
-          band_load<M, 1>(f, plan.ver, b, d, -1, 1, (unsigned)s + 1u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1,
-                          err, plan.poll_ns);
+          band_load<M, 1>(f, plan.ver, b, d, -1, 1, RES ? 0u : (unsigned)s + 1u, smem + LY::HALO, 1,
+                          smem + LY::HALOP, 0, 1, err, plan.poll_ns);
         if (tid == 128) {
           s_stop = stop_now;
           if (plan.trace && 4 * task + 3 < plan.trace_cap) s_tr[2] += gtimer() - s_tr[3];
@@ -434,9 +501,9 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       if (tr) s_tr[6] += gtimer() - s_tr[3];
       if (s_stop) return;
     }
-    band_writeback<M>(f, b, dlast, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
+    if (!RES) band_writeback<M>(f, b, dlast, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
     __syncthreads();
-    if (warp == 4 && c < BW) {  // publish the last step
+    if (!RES && warp == 4 && c < BW) {  // publish the last step
       const int cl = b.cell(c, dlast);
       if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
     }

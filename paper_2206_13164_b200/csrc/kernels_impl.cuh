@@ -359,6 +359,7 @@ void poll_tuning(int* split_wait, int* poll_ns);
 void band_scratch(momg_field* f, unsigned** ver, unsigned** next);
 bool band_sweep_enabled();
 bool band2_enabled();
+bool band_residual_enabled();
 void set_band_mode(int m);
 const uint32_t* split_schedule(momg_field* f, int nsweeps, const int* dirs, int radius, int seg);
 
@@ -404,6 +405,31 @@ struct Launch {
     return need < 148 * 8 ? need : 148 * 8;
   }
   static void residual(const DevCtx& ctx, const momg_field* f, momg_field* out) {
+    if constexpr (use_split<M>()) {
+      if (ctx.order == 1 && band_sweep_enabled() && band_residual_enabled()) {
+        // the band kernel in residual mode: (band, diagonal chunk) tasks
+        static bool rattr = false;
+        if (!rattr) {
+          set_smem(sp::k5_band<M, 32, true>, sp::BandLayout<M>::bytes);
+          rattr = true;
+        }
+        sp::BandPlan bp{};
+        band_scratch(out, &bp.ver, &bp.next);
+        bp.nsweeps = 1;
+        bp.nbands = (f->nx + 31) / 32;
+        const int ndiag = std::min(31, f->nx - 1) + f->ny;
+        bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
+        bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
+        bp.nchunks = (ndiag + bp.clen - 1) / bp.clen;
+        const int tasks = bp.nbands * bp.nchunks;
+        const int nb = tasks < 148 ? tasks : 148;
+        DevCtx c = ctx;
+        sp::k5_band<M, 32, true><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(
+            f->dev(), c, momg_rt::err_dev(), bp, out->dev());
+        momg_rt::count_launch(1);
+        return;
+      }
+    }
     if constexpr (use_tc<M>()) {
       tc_attrs();
       const int g = tc_grid(f->nx * f->ny, tc::SEG);
@@ -479,7 +505,7 @@ struct Launch {
             bp.trace = trace_buffer(&bp.trace_cap);
             int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
             if (nb > bp.nsweeps * bp.nbands) nb = bp.nsweeps * bp.nbands;
-            sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp);
+            sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp, fd);
             momg_rt::count_launch(1);
             return;
           }

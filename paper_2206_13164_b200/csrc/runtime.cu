@@ -502,6 +502,16 @@ bool band_sweep_enabled() {
 }
 void set_band_mode(int m) { g_band = m; }
 
+// first-order residual on the band kernel (MOMG_BAND_RES=0: k3_residual)
+bool band_residual_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("MOMG_BAND_RES");
+    on = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // second-order / rhs sweeps on the 16-column band kernel (MOMG_BAND2=0: the
 // wavefront-item kernel k4_sweep)
 bool band2_enabled() {
