@@ -139,6 +139,12 @@ int momg_residual(const momg_ctx* ctx, const momg_field* field, momg_field* out,
    sweep_order nullable ({0,1,2,3}); evals += cell updates (WorkStats) */
 int momg_fast_sweep(const momg_ctx* ctx, momg_field* field, const momg_field* rhs,
                     const int* sweep_order, long long* evals, momg_err* err);
+/* fast_sweep_step (no rhs) followed by residual into `out`, the sequence of
+ * nmg_cycle (multigrid.cpp:170-176) and of the C5 step: identical results to
+ * the two calls, run as one launch (the residual follows the last sweep's
+ * wavefront on otherwise idle SMs) where the band kernels apply */
+int momg_fast_sweep_residual(const momg_ctx* ctx, momg_field* field, const int* sweep_order, momg_field* out,
+                             long long* evals, momg_err* err);
 /* euler_step (single_level.cpp:74-97) with residuals = R(field) evaluated inside */
 int momg_euler_step(const momg_ctx* ctx, momg_field* field, const momg_field* rhs, momg_err* err);
 /* total_mass / mass_correction (single_level.cpp:168-183) */

@@ -236,7 +236,12 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
   constexpr int EPT = (NE + THREADS - 1) / THREADS;  // per thread in the copy phase
   const int tid = threadIdx.x;
   const int warp = tid >> 5, g = warp / P, q = warp % P, c = tid & 31;
-  const int ntasks = RES ? plan.nchunks * plan.nbands : plan.nsweeps * plan.nbands;
+  // sweep tasks (sweep, band), then residual tasks (chunk, band): the
+  // standalone residual (RES) has only the latter; a fused sweep+residual
+  // launch (plan.nchunks > 0) appends them, polling for the final version
+  const int sweep_tasks = RES ? 0 : plan.nsweeps * plan.nbands;
+  const int ntasks = sweep_tasks + plan.nchunks * plan.nbands;
+  const unsigned rneed = RES ? 0u : (unsigned)plan.nsweeps;
   for (;;) {
     if (tid == 0) {
       s_task = (int)atomicAdd(plan.next, 1u);
@@ -245,8 +250,11 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     __syncthreads();
     const int task = s_task;
     if (task >= ntasks || s_stop) return;
-    const int s = RES ? 0 : task / plan.nbands, k = task % plan.nbands;
-    const int dir = RES ? 0 : (int)((plan.dirbits >> (2 * s)) & 3u);
+    const bool res = task >= sweep_tasks;  // uniform per task
+    const int rtask = task - sweep_tasks;
+    const int s = res ? plan.nsweeps - 1 : task / plan.nbands, k = (res ? rtask : task) % plan.nbands;
+    // residual tasks walk the frame of the last sweep, whose wavefront they follow
+    const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
     BandGeo b;
     b.nx = f.nx;
     b.ny = f.ny;
@@ -256,8 +264,8 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     b.j_up = dir == 0 || dir == 1;
     const int ir = BW * k + c;
     int dfirst = BW * k, dlast = min(BW * k + BW - 1, f.nx - 1) + f.ny - 1;
-    if (RES) {
-      dfirst += (task / plan.nbands) * plan.clen;
+    if (res) {
+      dfirst += (rtask / plan.nbands) * plan.clen;
       dlast = min(dlast, dfirst + plan.clen - 1);
       if (dfirst > dlast) {  // empty chunk of a partial band
         __syncthreads();
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     // prologue: warp 0 alone waits (with back-off) for the cells of the
     // first two diagonals and band k-1's halo cell, then every warp loads
     // OLD1 <- old(dfirst), X <- old(dfirst+1), HALO <- band k-1 at dfirst-1
-    if (!RES && warp == 0) {
+    if (!res && warp == 0) {
       for (int e = c; e < 2 * NS + 1; e += 32) {
         const int cl = e < 2 * NS ? b.cell(e % NS, dfirst + e / NS) : (k > 0 ? b.cell(-1, dfirst - 1) : -1);
         const unsigned need = e < 2 * NS ? (unsigned)s : (unsigned)s + 1u;
@@ -292,13 +300,17 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       }
     }
     __syncthreads();
-    band_load<M, 4>(f, plan.ver, b, dfirst, 0, NS, 0u, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp, 16, err, 0);
-    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, NS, 0u, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err, 0);
+    const unsigned pn = res ? rneed : 0u;  // sweep tasks polled above
+    band_load<M, 4>(f, plan.ver, b, dfirst, 0, NS, pn, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp, 16, err,
+                    kPrologueSleepNs);
+    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, NS, pn, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err,
+                    kPrologueSleepNs);
     if (k > 0 && warp == 15)
-      band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, 0u, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1, err, 0);
-    if (RES)  // a chunk may start mid-band: its upstream states are old(dfirst-1)
-      band_load<M, 2>(f, plan.ver, b, dfirst - 1, 0, BW, 0u, smem + LY::V_V * VEC, SPV, smem + LY::PV, warp, 16,
-                      err, 0);
+      band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, pn, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1, err,
+                      kPrologueSleepNs);
+    if (res)  // a chunk may start mid-band: its upstream states are old(dfirst-1)
+      band_load<M, 2>(f, plan.ver, b, dfirst - 1, 0, BW, pn, smem + LY::V_V * VEC, SPV, smem + LY::PV, warp, 16,
+                      err, kPrologueSleepNs);
     __syncthreads();
     if (warp == 4)
       band_pre<M, BW>(f, ctx, b, dfirst, smem + LY::V_OLD1 * VEC, smem + LY::PO, smem + LY::PRE + (dfirst & 1) * PRE_N * 32);
@@ -310,7 +322,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     for (int d = dfirst; d <= dlast; ++d) {
       if (tr) s_tr[3] = gtimer();
       // write-back of step d-1 (V is read here before (A) overwrites it)
-      if (!RES && d > dfirst) band_writeback<M>(f, b, d - 1, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
+      if (!res && d > dfirst) band_writeback<M>(f, b, d - 1, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
       // ---- (A) stage the step's face states.  Sources: OLD1 (own old
       // states), X (old states of diagonal d+1), V (= L of group 1: new
       // states of d-1) and HALO.  Every destination except group 1's L is
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       // ---- (C) face group 0: cell update (update_split); groups 1-3:
       // publish the previous step's cells, band k-1's new cell and old(d+2)
       // for the next step, update scalars of d+1
-      if (RES && g == 0) {
+      if (res && g == 0) {
         // residual: R = Q - sum of the face fluxes into D (group 1's U) and
         // V <- S (old states of d for the next diagonal's upstream faces)
         const double* pre = smem + LY::PRE + (d & 1) * PRE_N * 32 + c;
@@ -477,19 +489,19 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         // publish step d-1: its write-back happened before the last CTA
         // barrier, so this release orders it (fence cumulativity) and the
         // update's critical path carries no memory fence
-        if (!RES && wi == 0 && d > dfirst && c < BW) {
+        if (!res && wi == 0 && d > dfirst && c < BW) {
           const int cl = b.cell(c, d - 1);
           if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
         }
         if (d + 1 <= dlast)
-          band_load<M, 4>(f, plan.ver, b, d + 2, 0, NS, (unsigned)s, smem + LY::V_X * VEC, SPV, smem + LY::PX, wi,
-                          12, err, plan.poll_ns);
+          band_load<M, 4>(f, plan.ver, b, d + 2, 0, NS, res ? rneed : (unsigned)s, smem + LY::V_X * VEC, SPV,
+                          smem + LY::PX, wi, 12, err, plan.poll_ns);
         if (wi == 0 && d + 1 <= dlast)  // OLD1 / PO hold diagonal d+1 since (A)
           band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
                           smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         // band k-1's new cell last: by then it is (nearly always) published
         if (k > 0 && wi == 11 && d + 1 <= dlast)
-          band_load<M, 1>(f, plan.ver, b, d, -1, 1, RES ? 0u : (unsigned)s + 1u, smem + LY::HALO, 1,
+          band_load<M, 1>(f, plan.ver, b, d, -1, 1, res ? rneed : (unsigned)s + 1u, smem + LY::HALO, 1,
                           smem + LY::HALOP, 0, 1, err, plan.poll_ns);
         if (tid == 128) {
           s_stop = stop_now;
@@ -501,9 +513,9 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       if (tr) s_tr[6] += gtimer() - s_tr[3];
       if (s_stop) return;
     }
-    if (!RES) band_writeback<M>(f, b, dlast, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
+    if (!res) band_writeback<M>(f, b, dlast, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
     __syncthreads();
-    if (!RES && warp == 4 && c < BW) {  // publish the last step
+    if (!res && warp == 4 && c < BW) {  // publish the last step
       const int cl = b.cell(c, dlast);
       if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
     }

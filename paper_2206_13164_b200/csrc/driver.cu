@@ -165,10 +165,17 @@ static void nmg_cycle(Hierarchy& h, int level, momg_field* field, const momg_fie
     *work += 4 * cells * pol.s3;
     return;
   }
-  sweeps(ctx, field, rhs, pol.s1);
-  *work += 4 * cells * pol.s1;
   LevelWork& w = h.work[level];
-  momg_gpu::op_residual(ctx, field, w.res.f);
+  if (!rhs && pol.s1 > 0) {
+    // finest level: the last pre-smoothing launch and the residual as one
+    // band launch (identical results; op_sweep_residual falls back)
+    sweeps(ctx, field, nullptr, pol.s1 - 1 - (pol.s1 - 1) % 4);
+    momg_gpu::op_sweep_residual(ctx, field, kCanon, w.res.f, (pol.s1 - 1) % 4 + 1);
+  } else {
+    sweeps(ctx, field, rhs, pol.s1);
+    momg_gpu::op_residual(ctx, field, w.res.f);
+  }
+  *work += 4 * cells * pol.s1;
   momg_gpu::op_defect(w.res.f, rhs, w.defect.f);
   momg_gpu::op_restrict_sol(field, w.coarse.f);
   momg_gpu::op_copy(w.before.f, w.coarse.f);

@@ -404,6 +404,51 @@ struct Launch {
     const int need = (work + per_block - 1) / per_block;
     return need < 148 * 8 ? need : 148 * 8;
   }
+  // fast_sweep_step followed by residual (nmg_cycle, multigrid.cpp:170-176)
+  // as ONE band launch: the residual tasks follow the last sweep's wavefront
+  // on the SMs the sweep's dependency DAG leaves idle.  Returns false when
+  // the fused path does not apply (the caller runs the two operations).
+  static bool sweep_res(const DevCtx& ctx, momg_field* f, const int* order, momg_field* out, int iters) {
+    if constexpr (use_split<M>()) {
+      if (ctx.order == 1 && iters >= 1 && iters <= 4 && persistent_sweep_enabled() && split_sweep_enabled() &&
+          band_sweep_enabled() && band_residual_enabled()) {
+        static bool battr = false;
+        if (!battr) {
+          set_smem(sp::k5_band<M, 32>, sp::BandLayout<M>::bytes);
+          battr = true;
+        }
+        sp::BandPlan bp{};
+        band_scratch(f, &bp.ver, &bp.next);
+        bp.nsweeps = 4 * iters;
+        bp.nbands = (f->nx + 31) / 32;
+        bp.dirbits = 0;
+        for (int s = 0; s < 16; ++s) {
+          bp.dirs[s] = order[s & 3];
+          bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
+        }
+        int sw = 0;
+        poll_tuning(&sw, &bp.poll_ns);
+        const int ndiag = std::min(31, f->nx - 1) + f->ny;
+        bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
+        bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
+        bp.nchunks = (ndiag + bp.clen - 1) / bp.clen;
+        int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
+        const int tasks = (bp.nsweeps + bp.nchunks) * bp.nbands;
+        if (nb > tasks) nb = tasks;
+        DevCtx c = ctx;
+        sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(
+            f->dev(), c, momg_rt::err_dev(), bp, out->dev());
+        momg_rt::count_launch(1);
+        return true;
+      }
+    }
+    (void)ctx;
+    (void)f;
+    (void)order;
+    (void)out;
+    (void)iters;
+    return false;
+  }
   static void residual(const DevCtx& ctx, const momg_field* f, momg_field* out) {
     if constexpr (use_split<M>()) {
       if (ctx.order == 1 && band_sweep_enabled() && band_residual_enabled()) {
@@ -503,6 +548,8 @@ struct Launch {
             poll_tuning(&sw, &bp.poll_ns);
             bp.exp = sw;
             bp.trace = trace_buffer(&bp.trace_cap);
+            bp.nchunks = 0;  // no fused residual tasks
+            bp.clen = 1;
             int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
             if (nb > bp.nsweeps * bp.nbands) nb = bp.nsweeps * bp.nbands;
             sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp, fd);
@@ -675,7 +722,7 @@ struct Launch {
     momg_rt::count_launch(1);
   }
   static const Ops* ops() {
-    static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial, sweep_n};
+    static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial, sweep_n, sweep_res};
     return &o;
   }
 };

@@ -580,6 +580,11 @@ void op_restrict_res(const momg_field* arrays, const momg_field* coarse, momg_fi
 void op_fas(momg_field* fine, const momg_field* before, const momg_field* after) {
   ops_for(fine->M)->fas(fine, before, after);
 }
+void op_sweep_residual(const DevCtx& ctx, momg_field* f, const int order[4], momg_field* out, int iters) {
+  if (ops_for(f->M)->sweep_res(ctx, f, order, out, iters)) return;
+  op_sweep_n(ctx, f, nullptr, order, iters);
+  op_residual(ctx, f, out);
+}
 void op_defect(const momg_field* res, const momg_field* rhs, momg_field* out) {
   if (!rhs) {
     const size_t cells = (size_t)res->nx * res->ny;
@@ -964,6 +969,19 @@ int momg_fast_sweep(const momg_ctx* ctx, momg_field* f, const momg_field* rhs,
   static const int canon[4] = {0, 1, 2, 3};
   const int* order = sweep_order ? sweep_order : canon;
   momg_gpu::op_sweep(momg_gpu::make_ctx(ctx), f, rhs, order);
+  const int rc = momg_rt::sync_check(err);
+  if (rc == MOMG_OK && evals) *evals += 4LL * f->nx * f->ny;
+  return rc;
+}
+
+int momg_fast_sweep_residual(const momg_ctx* ctx, momg_field* f, const int* sweep_order, momg_field* out,
+                             long long* evals, momg_err* err) {
+  CLEAR_ERR();
+  ENSURE();
+  if (!ctx || !f || !out || !same_shape(f, out)) return arg_error(err, "momg_fast_sweep_residual: shape mismatch");
+  if (!(ctx->knudsen > 0)) return config_error(err, "collision_frequency: Kn must be positive");
+  static const int canon[4] = {0, 1, 2, 3};
+  momg_gpu::op_sweep_residual(momg_gpu::make_ctx(ctx), f, sweep_order ? sweep_order : canon, out);
   const int rc = momg_rt::sync_check(err);
   if (rc == MOMG_OK && evals) *evals += 4LL * f->nx * f->ny;
   return rc;

@@ -60,6 +60,7 @@ struct Ops {
   void (*defect)(const momg_field*, const momg_field*, momg_field*);
   void (*norm_partial)(const momg_field*, const momg_field*, double*, int);
   void (*sweep_n)(const DevCtx&, momg_field*, const momg_field*, const int*, int);
+  bool (*sweep_res)(const DevCtx&, momg_field*, const int*, momg_field*, int);
 };
 const Ops* ops_for(int M);
 DevCtx make_ctx(const momg_ctx* c);
@@ -72,6 +73,8 @@ void field_free(momg_field* f);
 void op_residual(const DevCtx& ctx, const momg_field* f, momg_field* out);
 void op_sweep(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int order[4]);
 void op_sweep_n(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int order[4], int iters);
+// fast_sweep_step (no rhs) then residual into out, fused into one launch where possible
+void op_sweep_residual(const DevCtx& ctx, momg_field* f, const int order[4], momg_field* out, int iters = 1);
 void op_restrict_sol(const momg_field* fine, momg_field* coarse);
 void op_restrict_res(const momg_field* arrays, const momg_field* coarse, momg_field* out);
 void op_fas(momg_field* fine, const momg_field* before, const momg_field* after);

@@ -395,6 +395,23 @@ def fast_sweep_step(field: CellField, rhs: CellField | None, ctx: SolveContext,
     _raise(rc, err)
 
 
+def fast_sweep_residual(field: CellField, ctx: SolveContext, out: CellField | None = None,
+                        work: WorkStats | None = None, sweep_order=(0, 1, 2, 3)) -> CellField:
+    """fast_sweep_step (no rhs) then residual (the sequence of nmg_cycle,
+    multigrid.cpp:170-176), fused into one launch where the band kernels
+    apply; returns the residual field (params = cell params)."""
+    out = out or CellField(field.grid, field.order)
+    err = _Err()
+    c = ctx._c(field.order)
+    ev = C.c_longlong(0)
+    order = (C.c_int * 4)(*sweep_order)
+    rc = lib().momg_fast_sweep_residual(C.byref(c), field._h, order, out._h, C.byref(ev), C.byref(err))
+    if work is not None:
+        work.cell_evals += ev.value
+    _raise(rc, err)
+    return out
+
+
 def total_mass(field: CellField) -> float:
     v = C.c_double(0)
     err = _Err()

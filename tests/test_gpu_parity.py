@@ -145,6 +145,30 @@ def test_band_sweep_parity(M, model, nx, ny, order, with_rhs, space):
         assert np.max(np.abs(gp - wp)) < TOL
 
 
+@pytest.mark.parametrize("M,nx,ny,order", [(5, 70, 37, (0, 1, 2, 3)), (3, 33, 50, (2, 0, 3, 1)), (4, 9, 7, (1, 2, 3, 0))])
+def test_fused_sweep_residual(M, nx, ny, order):
+    """momg_fast_sweep_residual == fast_sweep_step then residual (bitwise), and
+    both against the oracle."""
+    g, octx, c, p = _setup(M, 1, SHAKHOV if M == 3 else BGK, nx, ny, True)
+    ctx = mctx(octx)
+    f1 = momg.CellField.from_host(mgrid(g), M, c, p)
+    momg.fast_sweep_step(f1, None, ctx, None, order)
+    r1 = momg.residual(f1, ctx)
+    f2 = momg.CellField.from_host(mgrid(g), M, c, p)
+    r2 = momg.fast_sweep_residual(f2, ctx, None, None, order)
+    a1, b1 = f1.download()
+    a2, b2 = f2.download()
+    np.testing.assert_array_equal(a1, a2)
+    np.testing.assert_array_equal(b1, b2)
+    rc1, rp1 = r1.download()
+    rc2, rp2 = r2.download()
+    np.testing.assert_array_equal(rc1, rc2)
+    np.testing.assert_array_equal(rp1, rp2)
+    wc, wp, _ = O.fast_sweep(octx, g, c, p, sweep_order=list(order))
+    assert rel_field(a2, wc) < TOL
+    assert rel_res(rc2, O.residual(octx, g, wc, wp)) < TOL
+
+
 def test_overlapped_transfers_double_buffer():
     """momg_field_{upload,download}_overlapped: a double-buffered stream of
     solves gives the same results as the synchronous path."""
