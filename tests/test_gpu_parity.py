@@ -169,6 +169,18 @@ def test_fused_sweep_residual(M, nx, ny, order):
     assert rel_res(rc2, O.residual(octx, g, wc, wp)) < TOL
 
 
+@pytest.mark.parametrize("M,model,nx,ny", [(5, BGK, 70, 37), (3, SHAKHOV, 40, 65), (4, BGK, 33, 9)])
+def test_band_residual_multiband(M, model, nx, ny):
+    """First-order residual on the band kernel (residual mode): several bands,
+    diagonal chunks starting mid-band, against the oracle."""
+    g, octx, c, p = _setup(M, 1, model, nx, ny, True)
+    want = O.residual(octx, g, c, p)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    got, gp = momg.residual(f, mctx(octx)).download()
+    assert rel_res(got, want) < TOL
+    np.testing.assert_array_equal(gp, p)
+
+
 def test_overlapped_transfers_double_buffer():
     """momg_field_{upload,download}_overlapped: a double-buffered stream of
     solves gives the same results as the synchronous path."""
