@@ -838,11 +838,7 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
 #pragma unroll
       for (int h = 0; h < (N + 31) / 32; ++h) {
         const int k = lane + 32 * h;
-#ifdef WB_PLAIN
-        if (k < N) dst[k] = Vb[k * SPV + cc];
-#else
         if (k < N) __stcg(dst + k, Vb[k * SPV + cc]);
-#endif
       }
     }
     // no fence here: the caller publishes the cells with st.release after a
