@@ -166,10 +166,11 @@ __device__ __forceinline__ int grad_normalize(double* v, P4& prm, double* bad) {
 // The transcendental part of the base row (one erfc, one exp per face):
 // a = -u_n / rs, g = e^{-a^2/2}/sqrt(2 pi), e0 = erfc(a/sqrt 2)/2.
 struct HalfBase {
-  double a, g, e0;
+  double a, g, e0, irs;
 };
 __device__ __forceinline__ HalfBase half_base(double un, double rs) {
   HalfBase h;
+  h.irs = 1.0 / rs;
   h.a = -un / rs;
   h.g = exp(-h.a * h.a * 0.5) * 0.3989422804014327;
   h.e0 = 0.5 * erfc(h.a * 0.7071067811865476);
@@ -194,9 +195,14 @@ __device__ __forceinline__ void half_kernels_b(double un, double rs, const HalfB
   he[1] = a;
 #pragma unroll
   for (int k = 1; k + 1 <= P; ++k) he[k + 1] = a * he[k] - (double)k * he[k - 1];
-  const double irs = 1.0 / rs;
+  const double irs = hb.irs;
   double prev[P + 1];  // column p-1 of the pairing table
   double fp = 1.0, rsp = 1.0;  // p!, rs^p
+  // 1/p! as compile-time constants (a multiplication instead of a division
+  // on the flux path; differs from rsp / p! by at most one rounding)
+  constexpr double kInvFact[9] = {1.0, 1.0, 0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0, 1.0 / 720.0, 1.0 / 5040.0,
+                                  1.0 / 40320.0};
+  static_assert(M <= 8, "kInvFact covers M <= 8");
 #pragma unroll
   for (int p = 0; p <= M; ++p) {
     double col[P + 1];
@@ -210,7 +216,7 @@ __device__ __forceinline__ void half_kernels_b(double un, double rs, const HalfB
       fp *= (double)p;
       rsp *= rs;
     }
-    double scale = rsp / fp;
+    double scale = rsp * kInvFact[p];
 #pragma unroll
     for (int m = 0; m <= M; ++m) {
       const double lo_m = (m == p ? fp : 0.0) - col[m];
