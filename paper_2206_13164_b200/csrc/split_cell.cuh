@@ -160,8 +160,11 @@ __device__ __forceinline__ void full_flux(int q, const double* s, double* o, dou
 #undef SP_FULL
 }
 
+// (one reciprocal of the density, shared by the callers after CSE: no
+// divisions on the face / update critical path; differences from the
+// reference's divisions are single roundings)
 __device__ __forceinline__ double rep_u32(const double* v, const P4& p, int axis) {
-  return p.v[axis] + v[(1 + axis) * SPV] / v[0];
+  return p.v[axis] + v[(1 + axis) * SPV] * (1.0 / v[0]);
 }
 __device__ __forceinline__ double rep_theta32(const double* v, const P4& p) {
   const double rho = v[0];
@@ -173,7 +176,8 @@ __device__ __forceinline__ double rep_theta32(const double* v, const P4& p) {
   fe2 += c2 * c2;
   trace += v[9 * SPV];
   fe2 += c3 * c3;
-  return p.v[3] + (2.0 * trace - fe2 / rho) / (3.0 * rho);
+  const double ir = 1.0 / rho;
+  return p.v[3] + (2.0 * trace - fe2 * ir) * (ir * (1.0 / 3.0));
 }
 __device__ __forceinline__ double grad_defect32(const double* v) {
   double defect = 0.0, trace = 0.0;
@@ -184,7 +188,7 @@ __device__ __forceinline__ double grad_defect32(const double* v) {
   defect = tc::smax(defect, fabs(v[3 * SPV]));
   trace += v[9 * SPV];
   defect = tc::smax(defect, fabs(trace));
-  return defect / fabs(v[0]);
+  return defect * fabs(1.0 / v[0]);
 }
 
 template <int M>
@@ -442,8 +446,8 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, int ax
       rs = sqrt(wb.v[3]);
     }
   } else if (branch == B_HALF) {
-    const double ul = (axis == 0 ? lp.v[0] : lp.v[1]) + L[(1 + axis) * SPV] / L[0];
-    const double ur = (axis == 0 ? rp.v[0] : rp.v[1]) + U[(1 + axis) * SPV] / U[0];
+    const double ul = (axis == 0 ? lp.v[0] : lp.v[1]) + L[(1 + axis) * SPV] * (1.0 / L[0]);
+    const double ur = (axis == 0 ? rp.v[0] : rp.v[1]) + U[(1 + axis) * SPV] * (1.0 / U[0]);
     const double cl = ctx.c_bound * sqrt(rep_theta32(L, lp));
     const double cr = ctx.c_bound * sqrt(rep_theta32(U, rp));
     const double lminus = tc::smin(ul - cl, ur - cr);

@@ -171,7 +171,7 @@ struct HalfBase {
 __device__ __forceinline__ HalfBase half_base(double un, double rs) {
   HalfBase h;
   h.irs = 1.0 / rs;
-  h.a = -un / rs;
+  h.a = -un * h.irs;
   h.g = exp(-h.a * h.a * 0.5) * 0.3989422804014327;
   h.e0 = 0.5 * erfc(h.a * 0.7071067811865476);
   return h;
