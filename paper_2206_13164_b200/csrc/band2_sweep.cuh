@@ -268,26 +268,28 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
           const double* ddx = axis == 0 ? f.dx : f.dy;
           double aL = 0.0, aU = 0.0;
           bool recl = false, recu = false;
+          // one reciprocal per slope denominator (no divisions on the
+          // staging path; single-rounding differences from face_split)
           if (rl) {
-            const double hl = xc[pl + 1] - xc[pl - 1], offL = 0.5 * ddx[pl];
+            const double ihl = 1.0 / (xc[pl + 1] - xc[pl - 1]), offL = 0.5 * ddx[pl];
             P4 w;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) w.v[t] = pL.v[t] + offL * ((pU.v[t] - pll4[t]) / hl);
+            for (int t = 0; t < 4; ++t) w.v[t] = pL.v[t] + offL * ((pU.v[t] - pll4[t]) * ihl);
             if (w.v[3] > 0.0) {
               recl = true;
               lp = w;
-              aL = offL / hl;
+              aL = offL * ihl;
             }
           }
           if (ru) {
-            const double hu = xc[pu + 1] - xc[pu - 1], offU = -0.5 * ddx[pu];
+            const double ihu = 1.0 / (xc[pu + 1] - xc[pu - 1]), offU = -0.5 * ddx[pu];
             P4 w;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) w.v[t] = pU.v[t] + offU * ((puu4[t] - pL.v[t]) / hu);
+            for (int t = 0; t < 4; ++t) w.v[t] = pU.v[t] + offU * ((puu4[t] - pL.v[t]) * ihu);
             if (w.v[3] > 0.0) {
               recu = true;
               rp = w;
-              aU = offU / hu;
+              aU = offU * ihu;
             }
           }
           const int klo = (q * Gen<M>::N) / P, khi = ((q + 1) * Gen<M>::N) / P;
