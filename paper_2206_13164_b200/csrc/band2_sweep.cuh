@@ -97,7 +97,8 @@ __device__ __forceinline__ int b2_update(const DevCtx& ctx, int q, bool valid, b
       SP_DISPATCH(q, B2_RS)
 #undef B2_RS
     }
-    gbar(0);
+    // at attempt 0 the barrier after the assembly already ordered V
+    if (attempt == 1) gbar(0);
     for (int iter = 0; iter <= 30; ++iter) {
       bool need = false;
       P4 to = prm;

@@ -765,7 +765,8 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
       SP_DISPATCH(q, SP_RS)
 #undef SP_RS
     }
-    gbar(0);
+    // at attempt 0 the barrier after the assembly already ordered V
+    if (attempt == 1) gbar(0);
     for (int iter = 0; iter <= 30; ++iter) {
       bool need = false;
       P4 to = prm;
