@@ -472,38 +472,77 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
 #pragma unroll
           for (int t = 0; t < 4; ++t) smem[LY::PV + c * 4 + t] = cp.v[t];
         }
-      } else if (g == 0) {
+      } else if (!res && g <= 1) {
+        // residual assembly (update_split's first half) on face groups 0 and 1,
+        // each taking half of every partition's elements; then group 0 updates.
+        // Group 1 first publishes step d-1 (its write-back happened before the
+        // last CTA barrier, so this release orders it: fence cumulativity; the
+        // earlier the publication, the shorter band k+1's halo wait)
+        if (g == 1 && q == 0 && d > dfirst && c < BW) {
+          const int cl = b.cell(c, d - 1);
+          if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
+        }
+        {
+          const double* pre = smem + LY::PRE + (d & 1) * PRE_N * 32 + c;
+          if (valid && (int)pre[PRE_FAIL * 32] == W_NONE) {
+            const double qv[3] = {pre[PRE_Q0 * 32], pre[PRE_Q0 * 32 + 32], pre[PRE_Q0 * 32 + 64]};
+            double* S = smem + LY::V_S * VEC + c;
+            double* V = smem + LY::V_V * VEC + c;
+#define B8_AS(Q)                                                                                                \
+  {                                                                                                             \
+    using PQ = Part<M, Q>;                                                                                      \
+    if (g == 0)                                                                                                 \
+      PQ::template assemble<0, PQ::CNT / 2>(S, nullptr, smem + 2 * VEC + c, smem + 5 * VEC + c,               \
+                                            smem + 8 * VEC + c, smem + 11 * VEC + c, pre[PRE_NU * 32],        \
+                                            ctx.collision == 2, ctx.shakhov_w, qv, pre[PRE_IDX * 32],         \
+                                            pre[PRE_IDY * 32], pre[PRE_DT * 32], false, V + VEC, V);          \
+    else                                                                                                        \
+      PQ::template assemble<PQ::CNT / 2, PQ::CNT>(S, nullptr, smem + 2 * VEC + c, smem + 5 * VEC + c,         \
+                                                  smem + 8 * VEC + c, smem + 11 * VEC + c, pre[PRE_NU * 32],  \
+                                                  ctx.collision == 2, ctx.shakhov_w, qv, pre[PRE_IDX * 32],   \
+                                                  pre[PRE_IDY * 32], pre[PRE_DT * 32], false, V + VEC, V);    \
+  }
+            SP_DISPATCH(q, B8_AS)
+#undef B8_AS
+          }
+          asm volatile("barrier.cta.sync 6, 256;" ::: "memory");  // groups 0 and 1
+        }
+        if (g == 1 && q == 1 && d + 1 <= dlast)  // OLD1 / PO hold diagonal d+1 since (A)
+          band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
+                          smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
+      }
+      if (!res && g == 0) {
         double bad = 0.0;
         P4 np = cp;
         const int w = update_split<M>(f, nullptr, ctx, q, valid, i, j, smem, &bad, cp, dxi, dyj, &np,
-                                      tr ? s_tr + 3 : nullptr, smem + LY::PRE + (d & 1) * PRE_N * 32 + c, s_ok);
+                                      tr ? s_tr + 3 : nullptr, smem + LY::PRE + (d & 1) * PRE_N * 32 + c, s_ok,
+                                      true);
         if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
         if (tr) s_tr[7] += gtimer() - s_tr[3];
         if (q == 0 && c < BW) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) smem[LY::PV + c * 4 + t] = np.v[t];
         }
-      } else {
-        const int wi = warp - 4;
-        const int stop_now = tid == 128 ? band_stop(err) : 0;  // issued early, consumed last
+      } else if (res ? g >= 1 : g >= 2) {
+        // prefetch warps: groups 1-3 in residual mode, 2-3 in the sweep
+        const int pw0 = res ? 4 : 8, npw = 16 - pw0;
+        const int wi = warp - pw0;
+        const int stop_now = wi == 0 && c == 0 ? band_stop(err) : 0;  // issued early, consumed last
         // publish step d-1: its write-back happened before the last CTA
         // barrier, so this release orders it (fence cumulativity) and the
         // update's critical path carries no memory fence
-        if (!res && wi == 0 && d > dfirst && c < BW) {
-          const int cl = b.cell(c, d - 1);
-          if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
-        }
+
         if (d + 1 <= dlast)
-          band_load<M, 4>(f, plan.ver, b, d + 2, 0, NS, res ? rneed : (unsigned)s, smem + LY::V_X * VEC, SPV,
-                          smem + LY::PX, wi, 12, err, plan.poll_ns);
-        if (wi == 0 && d + 1 <= dlast)  // OLD1 / PO hold diagonal d+1 since (A)
+          band_load<M, 5>(f, plan.ver, b, d + 2, 0, NS, res ? rneed : (unsigned)s, smem + LY::V_X * VEC, SPV,
+                          smem + LY::PX, wi, npw, err, plan.poll_ns);
+        if (res && wi == 0 && d + 1 <= dlast)  // (the sweep: group 1 does this)
           band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
                           smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         // band k-1's new cell last: by then it is (nearly always) published
-        if (k > 0 && wi == 11 && d + 1 <= dlast)
+        if (k > 0 && wi == npw - 1 && d + 1 <= dlast)
           band_load<M, 1>(f, plan.ver, b, d, -1, 1, res ? rneed : (unsigned)s + 1u, smem + LY::HALO, 1,
                           smem + LY::HALOP, 0, 1, err, plan.poll_ns);
-        if (tid == 128) {
+        if (wi == 0 && c == 0) {
           s_stop = stop_now;
           if (plan.trace && 4 * task + 3 < plan.trace_cap) s_tr[2] += gtimer() - s_tr[3];
         }

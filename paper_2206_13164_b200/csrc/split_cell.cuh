@@ -264,13 +264,15 @@ struct Part {
   }
   // residual assembly (spatial.cpp:127-132, collision.hpp:120-127), update_delta
   // (single_level.cpp:64-70) and f + dt delta (apply_update :47)
+  // elements [LO + KB, LO + KE) of the partition (default: all of them)
+  template <int KB = 0, int KE = CNT>
   static __device__ __forceinline__ void assemble(const double* S, const double* RH, const double* Fxm,
                                                   const double* Fxp, const double* Fym, const double* Fyp,
                                                   double nu, int shakhov, double shw, const double* qv,
                                                   double idx, double idy, double dt, bool rhs, double* D,
                                                   double* V) {
 #pragma unroll
-    for (int kk = 0; kk < CNT; ++kk) {
+    for (int kk = KB; kk < KE; ++kk) {
       constexpr int dummy = 0;
       (void)dummy;
       const int k = LO + kk;
@@ -703,7 +705,7 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
                                             int q, bool valid, int i, int j, double* base, double* bad,
                                             P4 cp, double dxi, double dyj, P4* new_p = nullptr,
                                             unsigned long long* dbg = nullptr, const double* pre = nullptr,
-                                            int* ok_out = nullptr) {
+                                            int* ok_out = nullptr, bool assembled = false) {
   // dbg (one thread, debug): [0] step start; accumulators [8] scalars,
   // [9] assembled, [10] normalize iterations, [11] normalized, [12] written
 #define US_STAMP(slot) \
@@ -740,16 +742,18 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
   US_STAMP(8);
   if (rhs) project1<M>(0, q, RH, rp, cp, valid && fail == W_NONE);
   const bool ok0 = valid && fail == W_NONE;
-  if (ok0) {
-    const double idx = pre ? pre[PRE_IDX * 32] : 1.0 / dxi, idy = pre ? pre[PRE_IDY * 32] : 1.0 / dyj;
-    const int shk = ctx.collision == 2;
-    const double shw = ctx.shakhov_w;
-    const bool hr = rhs != nullptr;
+  if (!assembled) {  // (the band sweep assembles on 8 warps before calling)
+    if (ok0) {
+      const double idx = pre ? pre[PRE_IDX * 32] : 1.0 / dxi, idy = pre ? pre[PRE_IDY * 32] : 1.0 / dyj;
+      const int shk = ctx.collision == 2;
+      const double shw = ctx.shakhov_w;
+      const bool hr = rhs != nullptr;
 #define SP_AS(Q) Part<M, Q>::assemble(S, RH, Fxm, Fxp, Fym, Fyp, nu, shk, shw, qv, idx, idy, dt, hr, D, V)
-    SP_DISPATCH(q, SP_AS)
+      SP_DISPATCH(q, SP_AS)
 #undef SP_AS
+    }
+    gbar(0);
   }
-  gbar(0);
   US_STAMP(9);
   // apply_update with the dt/2 retry; grad_normalize loop uniform per group
   bool done = !ok0;
