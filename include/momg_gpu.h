@@ -145,8 +145,12 @@ int momg_fast_sweep(const momg_ctx* ctx, momg_field* field, const momg_field* rh
  * wavefront on otherwise idle SMs) where the band kernels apply */
 int momg_fast_sweep_residual(const momg_ctx* ctx, momg_field* field, const int* sweep_order, momg_field* out,
                              long long* evals, momg_err* err);
-/* euler_step (single_level.cpp:74-97) with residuals = R(field) evaluated inside */
-int momg_euler_step(const momg_ctx* ctx, momg_field* field, const momg_field* rhs, momg_err* err);
+/* euler_step (single_level.cpp:74-97; single_level.hpp:55-58): f += dt (R - rhs)
+   with the single global dt (global_dt, :31-38), re-normalisation and the dt/2
+   retry.  residuals = residual(field) on the incoming field (nullable: evaluated
+   here); rhs nullable (empty RhsField) */
+int momg_euler_step(const momg_ctx* ctx, momg_field* field, const momg_field* residuals,
+                    const momg_field* rhs, momg_err* err);
 /* total_mass / mass_correction (single_level.cpp:168-183) */
 int momg_total_mass(const momg_field* field, double* out, momg_err* err);
 int momg_mass_correction(momg_field* field, double target_mass, momg_err* err);

@@ -314,10 +314,16 @@ class Oracle:
                                           s2, s3, gamma, C.byref(w), C.byref(err)), err)
         return c, p, w.value
 
-    def euler_step(self, ctx: Ctx, g: Grid, coeffs, params):
+    def euler_step(self, ctx: Ctx, g: Grid, coeffs, params, rhs=None):
+        """residual + euler_step (single_level.cpp:74-97); rhs = (coeffs, params) or None."""
         c = _arr(coeffs).copy(); p = _arr(params).copy(); err = MoErr(); cc = ctx.c(); gg = g.c()
-        self._check(self.lib.mo_euler_step(C.byref(cc), C.byref(gg), _ptr(c), _ptr(p),
-                                           C.byref(err)), err)
+        if rhs is None:
+            self._check(self.lib.mo_euler_step(C.byref(cc), C.byref(gg), _ptr(c), _ptr(p),
+                                               C.byref(err)), err)
+        else:
+            self._check(self.lib.mo_euler_step_rhs(C.byref(cc), C.byref(gg), _ptr(c), _ptr(p),
+                                                   _ptr(_arr(rhs[0])), _ptr(_arr(rhs[1])),
+                                                   C.byref(err)), err)
         return c, p
 
     def solve_steady(self, ctx: Ctx, g: Grid, coeffs, params, solver=NMG, tol=1e-8,

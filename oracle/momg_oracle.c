@@ -818,17 +818,26 @@ static int global_dt(const mo_ctx* ctx, const fieldv* f, double* dt_out, mo_err*
   return MO_OK;
 }
 
-/* euler_step, single_level.cpp:74-97 (empty rhs) */
-static int euler_step(const mo_ctx* ctx, fieldv* f, const double* res, mo_err* err) {
+/* euler_step, single_level.cpp:74-97 (rhs_c == NULL: empty rhs) */
+static int euler_step_rhs(const mo_ctx* ctx, fieldv* f, const double* res, const double* rhs_c,
+                          const double* rhs_p, mo_err* err) {
   double dt;
   TRY(global_dt(ctx, f, &dt, err));
   const iset* s = f->s;
-  for (int j = 0; j < f->g->ny; ++j)
-    for (int i = 0; i < f->g->nx; ++i) {
+  double* delta = (double*)malloc(sizeof(double) * s->n);
+  int rc = MO_OK;
+  for (int j = 0; j < f->g->ny && rc == MO_OK; ++j)
+    for (int i = 0; i < f->g->nx && rc == MO_OK; ++i) {
       const size_t k = CELL(f, i, j);
-      TRY(apply_update(s, f->c + k * s->n, f->p + k * 4, res + k * s->n, dt, i, j, err));
+      rc = update_delta(s, f->p + k * 4, res + k * s->n, rhs_c ? rhs_c + k * s->n : NULL,
+                        rhs_c ? rhs_p + k * 4 : NULL, delta, err);
+      if (rc == MO_OK) rc = apply_update(s, f->c + k * s->n, f->p + k * 4, delta, dt, i, j, err);
     }
-  return MO_OK;
+  free(delta);
+  return rc;
+}
+static int euler_step(const mo_ctx* ctx, fieldv* f, const double* res, mo_err* err) {
+  return euler_step_rhs(ctx, f, res, NULL, NULL, err);
 }
 int mo_euler_step(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
                   mo_err* err) {
@@ -837,6 +846,17 @@ int mo_euler_step(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* p
   double* res = (double*)malloc(sizeof(double) * (size_t)g->nx * g->ny * f.s->n);
   int rc = residual(ctx, &f, res, err);
   if (rc == MO_OK) rc = euler_step(ctx, &f, res, err);
+  free(res);
+  return rc;
+}
+
+int mo_euler_step_rhs(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
+                      const double* rhs_coeffs, const double* rhs_params, mo_err* err) {
+  clear(err);
+  fieldv f = {g, get_set(ctx->M), coeffs, params};
+  double* res = (double*)malloc(sizeof(double) * (size_t)g->nx * g->ny * f.s->n);
+  int rc = residual(ctx, &f, res, err);
+  if (rc == MO_OK) rc = euler_step_rhs(ctx, &f, res, rhs_coeffs, rhs_params, err);
   free(res);
   return rc;
 }

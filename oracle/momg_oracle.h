@@ -137,6 +137,9 @@ int mo_sweep_cells(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* 
                    mo_err* err);
 int mo_euler_step(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
                   mo_err* err);
+/* euler_step with an rhs (single_level.cpp:74-97, update_delta :63-70); rhs nullable */
+int mo_euler_step_rhs(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
+                      const double* rhs_coeffs, const double* rhs_params, mo_err* err);
 
 #ifdef __cplusplus
 }

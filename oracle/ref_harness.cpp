@@ -428,4 +428,18 @@ int mo_euler_step(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* p
   return rc;
 }
 
+int mo_euler_step_rhs(const mo_ctx* ctx, const mo_grid* g, double* coeffs, double* params,
+                      const double* rhs_coeffs, const double* rhs_params, mo_err* err) {
+  const SolveContext c = context(ctx);
+  CellField f = field(grid(g), ctx->M, coeffs, params);
+  RhsField rhs;
+  if (rhs_coeffs) rhs = arrays(ctx->M, f.size(), rhs_coeffs, rhs_params);
+  const int rc = guarded(err, [&] {
+    const auto r = residual(f, c.walls, c.model, c.gas, c.scheme, c.threads);
+    euler_step(f, r, rhs, c);
+  });
+  put_field(f, coeffs, params);
+  return rc;
+}
+
 }  // extern "C"

@@ -217,6 +217,7 @@ int momg_nmg_cycle(const momg_ctx* ctx, momg_field* field, int levels, int s1, i
     if (err) err->code = MOMG_ERR_ARG;
     return MOMG_ERR_ARG;
   }
+  momg_rt::acquire(field);
   try {
     Hierarchy h = prepare(field, levels);
     Cycle pol{s1, s2, s3, gamma};
@@ -255,9 +256,9 @@ int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_
   const int cap = opts->max_iterations > 0 ? opts->max_iterations : (opts->kind == 2 ? 200 : 100000);
   const momg_gpu::DevCtx dctx = momg_gpu::make_ctx(ctx);
   long long work = 0;
+  momg_rt::acquire(field);
   try {
     if (!(ctx->knudsen > 0)) throw Fail(MOMG_CONFIG, "collision_frequency: Kn must be positive");
-    if (opts->kind == 0) throw Fail(MOMG_CONFIG, "solve_steady: Euler is not on the device path");
     momg_err e{};
     FieldPtr res = make_field(grid_of(field), field->M);
     momg_gpu::op_residual(dctx, field, res.f);
@@ -281,7 +282,11 @@ int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_
       int step_rc = MOMG_OK;
       std::string step_msg;
       try {
-        if (opts->kind == 1) {
+        if (opts->kind == 0) {
+          // euler_step(field, res, {}, ctx) with res = R(field) of the previous iteration
+          momg_gpu::op_global_dt(dctx, field);
+          momg_gpu::op_euler(field, res.f, nullptr);
+        } else if (opts->kind == 1) {
           momg_gpu::op_sweep(dctx, field, nullptr, kCanon);
           work += 4LL * field->nx * field->ny;
         } else {
@@ -334,12 +339,43 @@ int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_
   }
 }
 
-int momg_euler_step(const momg_ctx*, momg_field*, const momg_field*, momg_err* err) {
-  if (err) {
-    err->code = MOMG_CONFIG;
-    std::snprintf(err->msg, sizeof(err->msg), "euler_step: not on the device path (SURVEY §8(f) row 3)");
+// euler_step (single_level.cpp:74-97): global_dt reduction, then the
+// per-cell forward-Euler update with the dt/2 retry; residuals nullable
+// (R(field) is evaluated first, as solve_steady passes it)
+int momg_euler_step(const momg_ctx* ctx, momg_field* field, const momg_field* residuals,
+                    const momg_field* rhs, momg_err* err) {
+  if (err) err->code = 0;
+  if (int rc = momg_rt::ensure(err)) return rc;
+  if (!ctx || !field || (residuals && (residuals->nx != field->nx || residuals->ny != field->ny ||
+                                        residuals->M != field->M)) ||
+      (rhs && (rhs->nx != field->nx || rhs->ny != field->ny || rhs->M != field->M)) || residuals == field ||
+      rhs == field) {
+    if (err) {
+      err->code = MOMG_ERR_ARG;
+      std::snprintf(err->msg, sizeof(err->msg), "momg_euler_step: shape mismatch or aliased arguments");
+    }
+    return MOMG_ERR_ARG;
   }
-  return MOMG_CONFIG;
+  momg_rt::acquire(field);
+  momg_rt::acquire(residuals);
+  momg_rt::acquire(rhs);
+  try {
+    if (!(ctx->knudsen > 0)) throw Fail(MOMG_CONFIG, "collision_frequency: Kn must be positive");
+    const momg_gpu::DevCtx dctx = momg_gpu::make_ctx(ctx);
+    FieldPtr own;
+    if (!residuals) {
+      own = make_field(grid_of(field), field->M);
+      momg_gpu::op_residual(dctx, field, own.f);
+      residuals = own.f;
+    }
+    momg_gpu::op_global_dt(dctx, field);
+    momg_gpu::op_euler(field, residuals, rhs);
+    momg_err e{};
+    check(momg_rt::sync_check(&e), e);
+    return MOMG_OK;
+  } catch (const Fail& f) {
+    return map_fail(f, err);
+  }
 }
 
 double momg_max_hermite_root(int degree) {

@@ -280,6 +280,67 @@ __global__ void __launch_bounds__(WPB * 32) k_defect(DevField res, DevField rhs,
   }
 }
 
+// ---------------------------------------------------------- euler_step
+// euler_step (single_level.cpp:74-97) for the warp-per-cell orders (7, 8):
+// one warp per cell, dt from the device global_dt reduction, the dt/2 retry
+// of apply_update (:44-61).
+template <int M>
+__global__ void __launch_bounds__(WPB * 32) k_euler(DevField f, DevField res, DevField rhs, int has_rhs,
+                                                    const double* dt_dev, DevErr* err) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const BlockView bv = block_setup<M, 1>(smem_raw, nullptr, &f, &res, &rhs, nullptr);
+  WarpBuf<M, 1>& sb = warp_buf<M, 1>(bv);
+  constexpr int T = Cfg<M>::T;
+  const int lane = lane_id();
+  const int cells = f.nx * f.ny;
+  for (int k = blockIdx.x * WPB + (threadIdx.x >> 5); k < cells; k += gridDim.x * WPB) {
+    if (err_set(err)) return;
+    const int i = k % f.nx, j = k / f.nx;
+    const double dt = ldg_cg(dt_dev);
+    load_cell_async<M>(&bv.hdr->f, k, sb.cell[0], sb.cp[0]);
+    load_cell_async<M>(&bv.hdr->g, k, sb.cell[1], sb.cp[1]);
+    __syncwarp();
+    double R[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) R[t] = sb.cell[1][item_pos<M>(t)];
+    if (has_rhs) {  // update_delta (single_level.cpp:63-70)
+      load_cell<M>(&bv.hdr->h, k, sb.UB, sb.par);
+      const P4 rp = p4(sb.par), cp = p4(sb.cp[0]);
+      proj_coeffs<M>(rp, cp, sb.c[1]);
+      __syncwarp();
+      double pr[T];
+      project_apply<M>(bv.tab, sb.UB, sb.Y1, sb.Y2, sb.c[1], pass_mask(rp, cp), pr);
+#pragma unroll
+      for (int t = 0; t < T; ++t) R[t] -= pr[t];
+    }
+    int w = W_NONE;
+    double bad = 0.0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const double step = attempt == 0 ? dt : 0.5 * dt;
+      double v[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) v[t] = fma(step, R[t], sb.cell[0][item_pos<M>(t)]);
+      __syncwarp();
+      store_items<M>(sb.X1, v);
+      if (lane < 4) sb.par[lane] = sb.cp[0][lane];
+      __syncwarp();
+      const double* rr;
+      w = grad_normalize<M, 1>(bv.tab, sb, sb.X1, sb.X2, sb.Y1, sb.par, v, &bad, &rr);
+      if (w == W_NONE) {
+        store_cell_regs<M>(&bv.hdr->f, k, v, sb.par);
+        __syncwarp();
+        break;
+      }
+      if (code_of(w) != E_NONPHYSICAL) break;
+    }
+    if (w != W_NONE) {
+      if (code_of(w) == E_NONPHYSICAL) w = W_DT_HALVING;
+      if (lane == 0) raise_err(err, code_of(w), w, i, j, bad);
+      return;
+    }
+  }
+}
+
 // ------------------------------------------------------------------- K6
 // residual_norm partials: block b sums the row-major cell chunk b of
 // area * sum_k alpha! theta^|alpha| R_k^2 in a fixed order (one warp per cell).
@@ -380,6 +441,7 @@ struct Launch {
     set_smem(k_restrict_res<M>, smem(1));
     set_smem(k_fas_correct<M>, smem(1));
     set_smem(k_defect<M>, smem(1));
+    set_smem(k_euler<M>, smem(1));
     done = true;
   }
   static void tc_attrs() {
@@ -397,6 +459,7 @@ struct Launch {
       set_smem(tc::k3_restrict_res<M>, s);
       set_smem(tc::k3_fas<M>, s);
       set_smem(tc::k3_defect<M>, s);
+      set_smem(tc::k3_euler<M>, s);
       done = true;
     }
   }
@@ -593,8 +656,8 @@ struct Launch {
           int nb = tc_sweep_blocks(kern, sp::Layout<M>::bytes, sp::THREADS);
           DevField fa = fd, ra = rd;
           void* args[] = {&fa, &ra, &has_rhs, &c, &err, &plan};
-          cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(sp::THREADS), args, sp::Layout<M>::bytes,
-                                      momg_rt::stream());
+          momg_rt::note_launch(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(sp::THREADS), args, sp::Layout<M>::bytes,
+                                      momg_rt::stream()));
           momg_rt::count_launch(1);
           return;
         }
@@ -607,8 +670,8 @@ struct Launch {
         int nb = tc_sweep_blocks(kern, tc::TSmem<M>::bytes);
         DevField fa = fd, ra = rd;
         void* args[] = {&fa, &ra, &has_rhs, &c, &err, &plan};
-        cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(tc::VS), args, tc::TSmem<M>::bytes,
-                                    momg_rt::stream());
+        momg_rt::note_launch(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(tc::VS), args, tc::TSmem<M>::bytes,
+                                    momg_rt::stream()));
         momg_rt::count_launch(1);
         return;
       }
@@ -716,13 +779,29 @@ struct Launch {
         momg_rt::err_dev());
     momg_rt::count_launch(1);
   }
+  // euler_step: dt_dev = device scalar of the global_dt reduction
+  static void euler(const momg_field* f_, const momg_field* res, const momg_field* rhs, const double* dt_dev) {
+    momg_field* f = const_cast<momg_field*>(f_);
+    if constexpr (use_tc<M>()) {
+      tc_attrs();
+      tc::k3_euler<M><<<tc_grid(f->nx * f->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(
+          f->dev(), res->dev(), rhs ? rhs->dev() : res->dev(), rhs != nullptr, dt_dev, momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
+    attrs();
+    k_euler<M><<<grid_blocks(f->nx * f->ny), WPB * 32, smem(1), momg_rt::stream()>>>(
+        f->dev(), res->dev(), rhs ? rhs->dev() : res->dev(), rhs != nullptr, dt_dev, momg_rt::err_dev());
+    momg_rt::count_launch(1);
+  }
   static void norm_partial(const momg_field* res, const momg_field* field, double* partial,
                            int blocks) {
     k_norm_partial<M><<<blocks, 256, 0, momg_rt::stream()>>>(res->dev(), field->dev(), partial);
     momg_rt::count_launch(1);
   }
   static const Ops* ops() {
-    static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial, sweep_n, sweep_res};
+    static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial, sweep_n, sweep_res,
+                          euler};
     return &o;
   }
 };

@@ -392,6 +392,61 @@ __global__ void __launch_bounds__(VS) k3_fas(DevField fine, DevField before, Dev
   }
 }
 
+// euler_step (single_level.cpp:74-97): f <- f + dt (R - project(rhs -> cell
+// basis)) with the global dt (device scalar from the global_dt reduction),
+// then grad_normalize; a nonphysical result is retried once at dt/2 from the
+// saved state (apply_update, :44-61), a second failure is SolverError(i, j).
+// Thread per cell; the saved state stays in HBM until the store.
+template <int M>
+__global__ void __launch_bounds__(VS) k3_euler(DevField f, DevField res, DevField rhs, int has_rhs,
+                                               const double* dt_dev, DevErr* err) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* base = reinterpret_cast<double*>(smem_raw);
+  constexpr int N = Gen<M>::N, NP = (N + 3) & ~3;
+  double* D = base + threadIdx.x;
+  double* V = base + (size_t)N * VS + threadIdx.x;
+  const int cells = f.nx * f.ny;
+  for (int k = blockIdx.x * VS + threadIdx.x; k < cells; k += gridDim.x * VS) {
+    if (err_on(err)) return;
+    const int i = k % f.nx, j = k / f.nx;
+    const double dt = __ldcg(dt_dev);
+    const P4 cp = ldp<false>(f.p + (size_t)k * 4);
+    const double* rc = res.c + (size_t)k * NP;
+    const double* fc = f.c + (size_t)k * NP;
+    // update_delta (single_level.cpp:63-70)
+    if (has_rhs) {
+      load_vec<M, false>(rhs.c + (size_t)k * NP, D);
+      project<M>(D, ldp<false>(rhs.p + (size_t)k * 4), cp);
+#pragma unroll
+      for (int q = 0; q < N; ++q) D[q * VS] = __ldg(rc + q) - D[q * VS];
+    } else {
+#pragma unroll
+      for (int q = 0; q < N; ++q) D[q * VS] = __ldg(rc + q);
+    }
+    int w = W_NONE;
+    double bad = 0.0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const double step = attempt == 0 ? dt : 0.5 * dt;
+#pragma unroll
+      for (int q = 0; q < N; ++q) V[q * VS] = fma(step, D[q * VS], __ldg(fc + q));
+      P4 prm = cp;
+      w = grad_normalize<M>(V, prm, &bad);
+      if (w == W_NONE) {
+        store_vec<M>(V, f.c + (size_t)k * NP);
+        __stcg(reinterpret_cast<double2*>(f.p + (size_t)k * 4), make_double2(prm.v[0], prm.v[1]));
+        __stcg(reinterpret_cast<double2*>(f.p + (size_t)k * 4) + 1, make_double2(prm.v[2], prm.v[3]));
+        break;
+      }
+      if (code_for(w) != E_NONPHYSICAL) break;  // plain Error propagates
+    }
+    if (w != W_NONE) {
+      if (code_for(w) == E_NONPHYSICAL) w = W_DT_HALVING;
+      raise(err, code_for(w), w, i, j, bad);
+      return;
+    }
+  }
+}
+
 // nmg_cycle's defect (multigrid.cpp:178-185)
 template <int M>
 __global__ void __launch_bounds__(VS) k3_defect(DevField res, DevField rhs, int has_rhs, DevField out,

@@ -83,9 +83,9 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
   for (int o = 16; o > 0; o >>= 1) v = smax(v, __shfl_down_sync(FULL, v, o));
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
   __syncthreads();
-  double t = 0.0;
+  double t = -INFINITY;
   if (threadIdx.x < 32) {
-    t = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : 0.0;
+    t = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : -INFINITY;
     for (int o = 16; o > 0; o >>= 1) t = smax(t, __shfl_down_sync(FULL, t, o));
   }
   return t;
@@ -124,16 +124,42 @@ __global__ void k_rscale_partial(DevField f, int NP, DevCtx ctx, double* partial
   if (threadIdx.x == 0) partial[blockIdx.x] = t;
 }
 
+// global_dt partials (single_level.cpp:31-38): max of -local_dt, so the
+// final max stage yields -min; a nonpositive temperature raises
+// NonphysicalState like local_dt (:20-21)
+__global__ void k_dt_partial(DevField f, DevCtx ctx, double* partial, DevErr* err) {
+  __shared__ double sh[32];
+  const int cells = f.nx * f.ny;
+  const int chunk = (cells + gridDim.x - 1) / gridDim.x;
+  const int lo = blockIdx.x * chunk, hi = min(cells, lo + chunk);
+  double v = -INFINITY;
+  for (int k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+    const int i = k % f.nx, j = k / f.nx;
+    const double ux = f.p[(size_t)k * 4], uy = f.p[(size_t)k * 4 + 1], theta = f.p[(size_t)k * 4 + 3];
+    if (!(theta > 0.0)) {
+      raise_err(err, E_NONPHYSICAL, W_DT_THETA, i, j, theta);
+      continue;
+    }
+    const double c = ctx.cfl_c_bound * sqrt(theta);
+    const double dt = ctx.cfl / ((fabs(ux) + c) / f.dx[i] + (fabs(uy) + c) / f.dy[j]);
+    v = smax(v, -dt);
+  }
+  const double t = block_max(v, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
 // final stage: out[0] = sum (or max) of partial[0..n); optional
 // out[1] = target / out[0] (mass correction factor); mode 0 sum, 1 max,
 // 2 sqrt(sum / area)
 __global__ void k_final(const double* partial, int n, int mode, double arg, double* out) {
   __shared__ double sh[32];
-  double v = 0.0;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) v = mode == 1 ? smax(v, partial[q]) : v + partial[q];
-  const double t = mode == 1 ? block_max(v, sh) : block_sum(v, sh);
+  // mode 3: max of negated values -> out[0] = -max (a minimum)
+  const bool mx = mode == 1 || mode == 3;
+  double v = mode == 3 ? -INFINITY : 0.0;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) v = mx ? smax(v, partial[q]) : v + partial[q];
+  const double t = mx ? block_max(v, sh) : block_sum(v, sh);
   if (threadIdx.x == 0) {
-    out[0] = mode == 2 ? sqrt(t / arg) : t;
+    out[0] = mode == 2 ? sqrt(t / arg) : mode == 3 ? -t : t;
     out[1] = arg / t;
   }
 }
@@ -157,7 +183,18 @@ static double* g_red = nullptr;       // partials [RED_BLOCKS] + out[4]
 static double* g_red_host = nullptr;  // pinned out[4]
 static std::atomic<long long> g_launches{0};
 
+static std::atomic<int> g_launch_err{0};  // first failed launch (cudaError_t)
 void count_launch(long long n) { g_launches += n; }
+void note_launch(cudaError_t e) {
+  int expected = 0;
+  if (e != cudaSuccess) g_launch_err.compare_exchange_strong(expected, (int)e);
+}
+void acquire(const momg_field* f) {
+  if (f && f->ready_pending) {
+    cudaStreamWaitEvent(g_stream, f->ev_ready, 0);
+    f->ready_pending = false;
+  }
+}
 long long launches() { return g_launches.load(); }
 cudaStream_t stream() { return g_stream; }
 DevErr* err_dev() { return g_err_dev; }
@@ -232,6 +269,15 @@ static const char* what_text(int w) {
 // Synchronises the stream and converts a device error record into *err
 // (then clears it).  Returns the status.
 int sync_check(momg_err* err) {
+  // a kernel that failed to launch (bad configuration, shared-memory
+  // attribute, cooperative grid too large) is an error, not a no-op
+  cudaError_t le = cudaGetLastError();
+  const int noted = g_launch_err.exchange(0);
+  if (le == cudaSuccess && noted) le = (cudaError_t)noted;
+  if (le != cudaSuccess) {
+    cudaStreamSynchronize(g_stream);
+    return cuda_check(le, err, "momg_gpu: kernel launch failed");
+  }
   cudaError_t e = cudaMemcpyAsync(g_err_host, g_err_dev, sizeof(DevErr), cudaMemcpyDeviceToHost,
                                   g_stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g_stream);
@@ -250,13 +296,21 @@ int sync_check(momg_err* err) {
 double* red_buf() { return g_red; }
 double* red_host() { return g_red_host; }
 
+static cudaStream_t g_own = nullptr;  // the library's own stream (kept for a switch back)
+// Switch the library stream: work still pending on the old stream is waited
+// for first, so nothing enqueued before the switch (field zero-fills, async
+// copies) can race with what follows on the new one.  NULL restores the
+// library's own stream.
 void set_stream(cudaStream_t s) {
   std::lock_guard<std::mutex> lock(g_mu);
-  if (g_own_stream && g_stream && s) {
-    cudaStreamDestroy(g_stream);
-    g_own_stream = false;
+  if (g_stream) cudaStreamSynchronize(g_stream);
+  if (g_own_stream && g_stream && !g_own) g_own = g_stream;
+  if (!s) {
+    if (!g_own) cudaStreamCreateWithFlags(&g_own, cudaStreamNonBlocking);
+    s = g_own;
   }
-  if (s) g_stream = s;
+  g_stream = s;
+  g_own_stream = s == g_own;
 }
 
 int init_device(int device, momg_err* err) {
@@ -635,6 +689,16 @@ void op_rscale(const DevCtx& ctx, const momg_field* f) {
                                              momg_rt::red_buf() + RED_BLOCKS);
   momg_rt::count_launch(2);
 }
+void op_global_dt(const DevCtx& ctx, const momg_field* f) {
+  k_dt_partial<<<RED_BLOCKS, RED_THREADS, 0, momg_rt::stream()>>>(f->dev(), ctx, momg_rt::red_buf(),
+                                                                   momg_rt::err_dev());
+  k_final<<<1, 1024, 0, momg_rt::stream()>>>(momg_rt::red_buf(), RED_BLOCKS, 3, 1.0,
+                                             momg_rt::red_buf() + RED_BLOCKS);
+  momg_rt::count_launch(2);
+}
+void op_euler(momg_field* f, const momg_field* residuals, const momg_field* rhs) {
+  ops_for(f->M)->euler(f, residuals, rhs, momg_rt::red_buf() + RED_BLOCKS);
+}
 // Fetches the reduction result (synchronising); also reports device errors.
 int fetch_scalar(double* out, momg_err* err) {
   cudaMemcpyAsync(momg_rt::red_host(), momg_rt::red_buf() + RED_BLOCKS, 2 * sizeof(double),
@@ -688,6 +752,10 @@ void field_free(momg_field* f) {
     cudaEventSynchronize(f->ev_free);
     cudaEventDestroy(f->ev_free);
   }
+  if (f->ev_ready) {
+    cudaEventSynchronize(f->ev_ready);
+    cudaEventDestroy(f->ev_ready);
+  }
   cudaFree(f->c);
   cudaFree(f->p);
   cudaFree(f->dgrid);
@@ -718,6 +786,13 @@ void field_free(momg_field* f) {
       err->msg[0] = 0;       \
     }                        \
   } while (0)
+
+// pending overlapped uploads of the fields an entry point touches
+static void ACQ(const momg_field* a, const momg_field* b = nullptr, const momg_field* c = nullptr) {
+  momg_rt::acquire(a);
+  momg_rt::acquire(b);
+  momg_rt::acquire(c);
+}
 
 static int arg_error(momg_err* err, const char* msg) {
   if (err) {
@@ -795,6 +870,7 @@ static int upload(momg_field* f, const double* coeffs, const double* params, mom
                   bool sync) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f);
   if (!f || !coeffs || !params) return arg_error(err, "momg_field_upload: null argument");
   const size_t cells = (size_t)f->nx * f->ny;
   // unpadded records (N % 4 == 0, e.g. M = 5): one linear copy (a pitched copy
@@ -815,6 +891,7 @@ static int download(const momg_field* f, double* coeffs, double* params, momg_er
                     bool sync) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f);
   if (!f) return arg_error(err, "momg_field_download: null field");
   const size_t cells = (size_t)f->nx * f->ny;
   cudaError_t e = cudaSuccess;
@@ -859,24 +936,34 @@ int momg_field_upload_overlapped(momg_field* f, const double* coeffs, const doub
   if (!f || !coeffs || !params) return arg_error(err, "momg_field_upload_overlapped: null argument");
   if (!copy_streams()) return momg_rt::cuda_check(cudaErrorUnknown, err, "momg_field_upload_overlapped");
   const size_t cells = (size_t)f->nx * f->ny;
-  cudaError_t e = cudaSuccess;
-  if (f->ev_free) e = cudaStreamWaitEvent(g_h2d, f->ev_free, 0);
+  // the copy must follow (a) the field's previous overlapped download and
+  // (b) everything already enqueued on the library stream (the zero-fill of
+  // a fresh field, kernels that used it); (b) costs nothing when the
+  // caller's compute calls have returned (they synchronise)
+  cudaEvent_t ev_lib = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&ev_lib, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev_lib, momg_rt::stream());
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(g_h2d, ev_lib, 0);
+  if (ev_lib) cudaEventDestroy(ev_lib);
+  if (e == cudaSuccess && f->ev_free) e = cudaStreamWaitEvent(g_h2d, f->ev_free, 0);
   if (e == cudaSuccess)
     e = f->NP == f->N ? cudaMemcpyAsync(f->c, coeffs, cells * f->N * sizeof(double), cudaMemcpyHostToDevice, g_h2d)
                       : cudaMemcpy2DAsync(f->c, f->NP * sizeof(double), coeffs, f->N * sizeof(double),
                                           f->N * sizeof(double), cells, cudaMemcpyHostToDevice, g_h2d);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(f->p, params, cells * 4 * sizeof(double), cudaMemcpyHostToDevice, g_h2d);
-  cudaEvent_t ev = nullptr;
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventRecord(ev, g_h2d);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(momg_rt::stream(), ev, 0);
-  if (ev) cudaEventDestroy(ev);  // released once complete
+  // deferred wait: the library stream waits for this copy only when an
+  // entry point first uses the field (momg_rt::acquire), so the upload of the
+  // next solve overlaps the compute of the current one
+  if (e == cudaSuccess && !f->ev_ready) e = cudaEventCreateWithFlags(&f->ev_ready, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(f->ev_ready, g_h2d);
+  if (e == cudaSuccess) f->ready_pending = true;
   return momg_rt::cuda_check(e, err, "momg_field_upload_overlapped");
 }
 int momg_field_download_overlapped(momg_field* f, double* coeffs, double* params, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f);
   if (!f || !coeffs || !params) return arg_error(err, "momg_field_download_overlapped: null argument");
   if (!copy_streams()) return momg_rt::cuda_check(cudaErrorUnknown, err, "momg_field_download_overlapped");
   const size_t cells = (size_t)f->nx * f->ny;
@@ -912,6 +999,7 @@ int momg_copy_barrier(momg_err* err) {
 int momg_field_copy(momg_field* dst, const momg_field* src, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(dst, src);
   if (!dst || !src || dst->nx != src->nx || dst->ny != src->ny || dst->M != src->M)
     return arg_error(err, "momg_field_copy: shape mismatch");
   momg_gpu::op_copy(dst, src);
@@ -921,6 +1009,7 @@ int momg_field_fill_maxwellian(momg_field* f, double rho, const double u[3], dou
                                momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f);
   if (!f) return arg_error(err, "momg_field_fill_maxwellian: null field");
   if (!(rho > 0.0) || !(theta > 0.0)) {
     if (err) {
@@ -954,7 +1043,9 @@ static int config_error(momg_err* err, const char* msg) {
 int momg_residual(const momg_ctx* ctx, const momg_field* f, momg_field* out, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f, out);
   if (!ctx || !same_shape(f, out)) return arg_error(err, "momg_residual: shape mismatch");
+  if (out == f) return arg_error(err, "momg_residual: out must not alias the field (residual returns a new vector)");
   if (!(ctx->knudsen > 0)) return config_error(err, "collision_frequency: Kn must be positive");
   momg_gpu::op_residual(momg_gpu::make_ctx(ctx), f, out);
   return momg_rt::sync_check(err);
@@ -964,7 +1055,9 @@ int momg_fast_sweep(const momg_ctx* ctx, momg_field* f, const momg_field* rhs,
                     const int* sweep_order, long long* evals, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f, rhs);
   if (!ctx || !f || (rhs && !same_shape(f, rhs))) return arg_error(err, "momg_fast_sweep: shape mismatch");
+  if (rhs == f) return arg_error(err, "momg_fast_sweep: rhs must not alias the field");
   if (!(ctx->knudsen > 0)) return config_error(err, "collision_frequency: Kn must be positive");
   static const int canon[4] = {0, 1, 2, 3};
   const int* order = sweep_order ? sweep_order : canon;
@@ -978,7 +1071,9 @@ int momg_fast_sweep_residual(const momg_ctx* ctx, momg_field* f, const int* swee
                              long long* evals, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f, out);
   if (!ctx || !f || !out || !same_shape(f, out)) return arg_error(err, "momg_fast_sweep_residual: shape mismatch");
+  if (out == f) return arg_error(err, "momg_fast_sweep_residual: out must not alias the field");
   if (!(ctx->knudsen > 0)) return config_error(err, "collision_frequency: Kn must be positive");
   static const int canon[4] = {0, 1, 2, 3};
   momg_gpu::op_sweep_residual(momg_gpu::make_ctx(ctx), f, sweep_order ? sweep_order : canon, out);
@@ -990,6 +1085,7 @@ int momg_fast_sweep_residual(const momg_ctx* ctx, momg_field* f, const int* swee
 int momg_total_mass(const momg_field* f, double* out, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f);
   if (!f) return arg_error(err, "momg_total_mass: null field");
   momg_gpu::op_mass(f, 1.0);
   return momg_gpu::fetch_scalar(out, err);
@@ -998,6 +1094,7 @@ int momg_total_mass(const momg_field* f, double* out, momg_err* err) {
 int momg_mass_correction(momg_field* f, double target, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f);
   if (!f) return arg_error(err, "momg_mass_correction: null field");
   double current = 0.0;
   momg_gpu::op_mass(f, target);
@@ -1017,6 +1114,7 @@ int momg_mass_correction(momg_field* f, double target, momg_err* err) {
 int momg_restrict_solution(const momg_field* fine, momg_field* coarse, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(fine, coarse);
   if (!pair_shape(fine, coarse))
     return config_error(err, "restrict_solution: grids are not a 2x2 refinement pair");
   momg_gpu::op_restrict_sol(fine, coarse);
@@ -1027,6 +1125,7 @@ int momg_restrict_residual(const momg_field* arrays, const momg_field* coarse, m
                            momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(arrays, coarse, out);
   if (!pair_shape(arrays, coarse) || !same_shape(coarse, out))
     return config_error(err, "restrict_residual: grids are not a 2x2 refinement pair");
   momg_gpu::op_restrict_res(arrays, coarse, out);
@@ -1037,6 +1136,7 @@ int momg_fas_correct(momg_field* fine, const momg_field* before, const momg_fiel
                      momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(fine, before, after);
   if (!pair_shape(fine, before) || !same_shape(before, after))
     return config_error(err, "fas_correct: grids are not a 2x2 refinement pair");
   momg_gpu::op_fas(fine, before, after);
@@ -1046,6 +1146,7 @@ int momg_fas_correct(momg_field* fine, const momg_field* before, const momg_fiel
 int momg_residual_norm(const momg_field* res, const momg_field* field, double* out, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(res, field);
   if (!same_shape(res, field)) return arg_error(err, "momg_residual_norm: shape mismatch");
   momg_gpu::op_norm(res, field);
   return momg_gpu::fetch_scalar(out, err);
@@ -1054,6 +1155,7 @@ int momg_residual_norm(const momg_field* res, const momg_field* field, double* o
 int momg_residual_scale(const momg_ctx* ctx, const momg_field* f, double* out, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(f);
   if (!ctx || !f) return arg_error(err, "momg_residual_scale: null argument");
   momg_gpu::op_rscale(momg_gpu::make_ctx(ctx), f);
   return momg_gpu::fetch_scalar(out, err);
@@ -1062,6 +1164,7 @@ int momg_residual_scale(const momg_ctx* ctx, const momg_field* f, double* out, m
 int momg_defect(const momg_field* res, const momg_field* rhs, momg_field* out, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(res, rhs, out);
   if (!same_shape(res, out) || (rhs && !same_shape(res, rhs)))
     return arg_error(err, "momg_defect: shape mismatch");
   momg_gpu::op_defect(res, rhs, out);
@@ -1071,6 +1174,7 @@ int momg_defect(const momg_field* res, const momg_field* rhs, momg_field* out, m
 int momg_axpy(momg_field* dst, const momg_field* src, momg_err* err) {
   CLEAR_ERR();
   ENSURE();
+  ACQ(dst, src);
   if (!same_shape(dst, src)) return arg_error(err, "momg_axpy: shape mismatch");
   momg_gpu::op_axpy(dst, src);
   return momg_rt::sync_check(err);

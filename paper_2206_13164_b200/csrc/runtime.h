@@ -24,6 +24,10 @@ struct momg_field {
   int* seg_plan32 = nullptr;        // split sweep (32-cell segments)
   struct Schedule* schedule = nullptr;  // split sweep: cached dependency-level item order
   cudaEvent_t ev_free = nullptr;        // overlapped transfers: last download of this field done
+  // overlapped upload pending on the H2D copy stream: the library stream
+  // waits on ev_ready the first time an entry point uses the field
+  mutable cudaEvent_t ev_ready = nullptr;
+  mutable bool ready_pending = false;
   DevField dev() const {
     DevField d;
     d.nx = nx;
@@ -47,6 +51,12 @@ cudaStream_t stream();
 momg_gpu::DevErr* err_dev();
 void count_launch(long long n);
 long long launches();
+// launch status of a kernel (cooperative launches return it; <<<>>> launches
+// are checked through cudaGetLastError): the first failure is kept and
+// reported as MOMG_ERR_CUDA by the next sync_check / fetch_scalar
+void note_launch(cudaError_t e);
+// make the library stream wait for a pending overlapped upload of f
+void acquire(const momg_field* f);
 }  // namespace momg_rt
 
 namespace momg_gpu {
@@ -61,6 +71,7 @@ struct Ops {
   void (*norm_partial)(const momg_field*, const momg_field*, double*, int);
   void (*sweep_n)(const DevCtx&, momg_field*, const momg_field*, const int*, int);
   bool (*sweep_res)(const DevCtx&, momg_field*, const int*, momg_field*, int);
+  void (*euler)(const momg_field*, const momg_field*, const momg_field*, const double*);
 };
 const Ops* ops_for(int M);
 DevCtx make_ctx(const momg_ctx* c);
@@ -85,5 +96,9 @@ void op_mass(const momg_field* f, double target);
 void op_scale_by_factor(momg_field* f);
 void op_norm(const momg_field* res, const momg_field* field);
 void op_rscale(const DevCtx& ctx, const momg_field* f);
+// global_dt (single_level.cpp:31-38): min local_dt, result left on the device
+void op_global_dt(const DevCtx& ctx, const momg_field* f);
+// euler_step (single_level.cpp:74-97) with the dt of the preceding op_global_dt
+void op_euler(momg_field* f, const momg_field* residuals, const momg_field* rhs);
 int fetch_scalar(double* out, momg_err* err);
 }  // namespace momg_gpu

@@ -170,8 +170,8 @@ struct PersistentSweep {
     DevErr* err = momg_rt::err_dev();
     DevCtx c = ctx;
     void* args[] = {&fd, &rd, &has_rhs, &c, &err, &plan};
-    cudaLaunchCooperativeKernel((void*)k_sweep_persistent<M, ORDER>, dim3(nb), dim3(PWPB * 32), args,
-                                smem(), momg_rt::stream());
+    momg_rt::note_launch(cudaLaunchCooperativeKernel((void*)k_sweep_persistent<M, ORDER>, dim3(nb), dim3(PWPB * 32), args,
+                                smem(), momg_rt::stream()));
     momg_rt::count_launch(1);
   }
 };

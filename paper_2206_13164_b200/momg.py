@@ -412,6 +412,17 @@ def fast_sweep_residual(field: CellField, ctx: SolveContext, out: CellField | No
     return out
 
 
+def euler_step(field: CellField, residuals: CellField | None, rhs: CellField | None,
+               ctx: SolveContext) -> None:
+    """single_level.cpp:74-97: f <- f + dt (R - rhs) with the single global dt
+    (global_dt, :31-38), re-normalisation and the dt/2 retry.  `residuals` =
+    residual(field, ctx) on the incoming field (None: evaluated here)."""
+    err = _Err()
+    c = ctx._c(field.order)
+    _raise(lib().momg_euler_step(C.byref(c), field._h, residuals._h if residuals is not None else None,
+                                 rhs._h if rhs is not None else None, C.byref(err)), err)
+
+
 def total_mass(field: CellField) -> float:
     v = C.c_double(0)
     err = _Err()

@@ -224,6 +224,32 @@ def test_transfer_ops_bitwise(R, M):
 
 
 @needs_ref
+@pytest.mark.parametrize("M,order,model", [(3, 1, BGK), (5, 2, SHAKHOV), (4, 1, ES_BGK)])
+def test_euler_step_bitwise(R, M, order, model):
+    """euler_step (single_level.cpp:74-97) with and without an rhs, and the
+    Euler solver of solve_steady, port vs reference bit for bit."""
+    g = Grid.uniform(7, 6, 1.0, 1.2)
+    ctx = cavity_ctx(M, order, model, kn=0.3, prandtl=2.0 / 3.0 if model != BGK else 1.0,
+                     bottom_theta=1.3)
+    c, p = smooth_field(g, M, seed=31 + M, uz=True)
+    a = P.euler_step(ctx, g, c, p)
+    b = R.euler_step(ctx, g, c, p)
+    _check_equal(a[0], b[0]); _check_equal(a[1], b[1])
+    rp = p.copy(); rp[:, 1] += 0.01; rp[:, 3] *= 1.03
+    rhs = (c * 1e-3, rp)
+    a = P.euler_step(ctx, g, c, p, rhs=rhs)
+    b = R.euler_step(ctx, g, c, p, rhs=rhs)
+    _check_equal(a[0], b[0]); _check_equal(a[1], b[1])
+    gg = Grid.uniform(8, 8)
+    cc, pp = uniform_field(gg, 3)
+    cx = cavity_ctx(3, 1, BGK, kn=0.1, lid=0.1)
+    a = P.solve_steady(cx, gg, cc, pp, solver=0, tol=1e-3)
+    b = R.solve_steady(cx, gg, cc, pp, solver=0, tol=1e-3)
+    assert a[2]["iterations"] == b[2]["iterations"] and a[2]["converged"]
+    _check_equal(a[0], b[0])
+
+
+@needs_ref
 def test_nmg_and_solve_bitwise(R):
     M = 3
     g = Grid.uniform(16, 16)
