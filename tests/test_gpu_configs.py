@@ -1,0 +1,126 @@
+"""GPU parity at BASELINE sizes the round-1 suite did not reach:
+
+* C3 (256^2, M=8, Shakhov Pr 2/3, Kn 0.01, second order, NMG over 5 levels)
+  and C4 (512^2, M=6, BGK, bottom wall theta=2, lid at rest, second order,
+  NMG over 6 levels): the iteration loop of solve_steady (multigrid.cpp:
+  243-320: nmg_cycle, mass_correction, residual, residual_norm) for one and
+  two V-cycles on the device, against the oracle's own run of the same loop
+  (tools/oracle_solve_ckpt.py -> tools/make_config_fixtures.py; the oracle
+  is bitwise-pinned to the reference, tests/test_oracle_pin.py).  Compared:
+  the residual ratio, the mass, per-row / per-column sums of the order<=3
+  moments, every coefficient of a 64-cell lattice and the basis params on
+  every 8th cell, at the per-sweep tolerance 1e-10 (relative to max(1,|f0|)).
+* C5-size band launches: one fused FS iteration + residual over 16 bands
+  (512^2, the bench kernel sp::k5_band<5,32>) against the oracle.
+* The grad_normalize iteration cap (projection.hpp:118-119) on the device.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import BGK, SHAKHOV, Grid, c5_field, cavity_ctx, count
+from oracle.api import MO_ERROR, Oracle, OracleError
+from test_gpu_parity import mctx, mgrid, rel_field, rel_res
+
+pytestmark = pytest.mark.gpu
+
+momg = pytest.importorskip("paper_2206_13164_b200.momg")
+O = Oracle("port")
+TOL = 1e-10
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+# name: (n, M, order, model, Kn, Pr, lid, bottom theta, levels)
+CONFIGS = {
+    "C3": (256, 8, 2, SHAKHOV, 0.01, 2.0 / 3.0, 0.1, 1.0, 5),
+    "C4": (512, 6, 2, BGK, 0.1, 1.0, 0.0, 2.0, 6),
+}
+
+
+def _device_loop(name, cycles):
+    n, M, order, model, kn, pr, lid, bt, levels = CONFIGS[name]
+    z = np.load(os.path.join(GOLD, f"{name}_it1.npz"))
+    octx = cavity_ctx(M, order, model, kn=kn, lid=lid, prandtl=pr, bottom_theta=bt)
+    octx.c_bound = octx.cfl_c_bound = float(z["c_bound"])
+    ctx = mctx(octx)
+    g = momg.Grid2D.uniform(n, n)
+    f = momg.uniform_field(g, M, 1.0, (0.0, 0.0, 0.0), 1.0)
+    r0 = momg.residual_norm(momg.residual(f, ctx), f)
+    target = momg.total_mass(f)
+    out = []
+    for _ in range(cycles):
+        momg.nmg_cycle(f, ctx, levels)
+        momg.mass_correction(f, target)
+        norm = momg.residual_norm(momg.residual(f, ctx), f)
+        out.append((norm / r0, norm, r0, momg.total_mass(f), f.download()))
+    return out
+
+
+def _check(name, tag, got):
+    z = np.load(os.path.join(GOLD, f"{name}_{tag}.npz"))
+    n = CONFIGS[name][0]
+    ratio, norm, r0, mass, (c, p) = got
+    assert abs(r0 - float(z["r0_norm"])) <= 1e-12 * float(z["r0_norm"])
+    assert abs(ratio - float(z["ratio"])) <= 1e-10 * float(z["ratio"])
+    assert abs(mass - float(z["mass"])) <= 1e-12
+    c3 = c.reshape(n, n, -1)
+    scale = np.maximum(1.0, np.abs(z["row_sums"][:, :1]))
+    assert np.max(np.abs(c3[:, :, :20].sum(axis=1) - z["row_sums"]) / scale) < TOL * n
+    scale = np.maximum(1.0, np.abs(z["col_sums"][:, :1]))
+    assert np.max(np.abs(c3[:, :, :20].sum(axis=0) - z["col_sums"]) / scale) < TOL * n
+    assert rel_field(c[z["cells"]], z["coeff_sub"]) < TOL
+    assert np.max(np.abs(p.reshape(n, n, 4)[::8, ::8] - z["params_sub"])) < TOL
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_config_vcycles_against_oracle(name):
+    got = _device_loop(name, 2)
+    _check(name, "it1", got[0])
+    if os.path.exists(os.path.join(GOLD, f"{name}_it2.npz")):
+        _check(name, "it2", got[1])
+
+
+def test_c5_fused_launch_16_bands():
+    """The bench kernel (fused FS iteration + residual, 32-column bands) on a
+    512^2 C5 field: 16 bands per sweep, four directions, residual tasks
+    appended; against the oracle's fast_sweep_step + residual."""
+    M, n = 5, 512
+    g = Grid.uniform(n, n)
+    octx = cavity_ctx(M, 1, BGK, kn=0.1, lid=0.0)
+    c, p = c5_field(n, n, M, seed=2206)
+    f = momg.CellField.from_host(mgrid(g), M, c, p)
+    r = momg.fast_sweep_residual(f, mctx(octx))
+    gc, gp = f.download()
+    rc, _ = r.download()
+    wc, wp, _ = O.fast_sweep(octx, g, c, p)
+    assert rel_field(gc, wc) < TOL and np.max(np.abs(gp - wp)) < TOL
+    assert rel_res(rc, O.residual(octx, g, wc, wp)) < TOL
+
+
+@pytest.mark.parametrize("M", [3, 5, 8])
+def test_grad_normalize_cap(M):
+    """Restricted reps whose order-1 / order-2 moments are ~1e3 / 1e6 times
+    the density: every re-projection leaves a rounding-level defect above
+    rel_tol 1e-12, so grad_normalize hits its 30-iteration cap and throws
+    momg::Error (not NonphysicalState) -- the oracle and the device alike."""
+    N = count(M)
+    fg = Grid.uniform(4, 6)
+    cg = fg.coarsen()
+    big = 1e3
+    c = np.zeros((fg.cells, N))
+    c[:, 0] = 1.0
+    c[:, 1] = big
+    c[:, 4] = big * big
+    c[:, 7] = 0.3 * big * big
+    c[:, 9] = 0.2 * big * big
+    c[5, 1] = 0.5
+    p = np.zeros((fg.cells, 4))
+    p[:, 3] = 1.0
+    with pytest.raises(OracleError) as e:
+        O.restrict_solution(M, fg, c, p, cg)
+    assert e.value.code == MO_ERROR and "iteration cap" in e.value.msg
+    fine = momg.CellField.from_host(mgrid(fg), M, c, p)
+    with pytest.raises(momg.Error) as ge:
+        momg.restrict_solution(fine, mgrid(cg))
+        momg.synchronize()
+    assert type(ge.value) is momg.Error
