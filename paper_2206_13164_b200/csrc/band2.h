@@ -17,6 +17,7 @@ struct Band2Plan {
   int order;       // 1 | 2
   int has_rhs;
   int poll_ns;
+  unsigned jitter;  // schedule perturbation seed (race stress tests; 0 = off)
 };
 }  // namespace sp
 struct DevCtx;

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
   const bool o2 = plan.order == 2;
   for (;;) {
     if (tid == 0) {
+      sched_jitter(plan.jitter, 1u);
       s_task = (int)atomicAdd(plan.next, 1u);
       s_stop = band_stop(err);
     }
@@ -337,12 +338,13 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
         const int wi = warp - 4;
         const int stop_now = tid == 128 ? band_stop(err) : 0;
         if (wi == 0 && d > dfirst && c < B2W) {
+          sched_jitter(plan.jitter, (unsigned)d);
           const int cl = b.cell(c, d - 1);
           if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
         }
         if (wi < 6 && d + 1 <= dlast)
           band_load<M, 3>(f, plan.ver, b, d + 3, 0, 18, (unsigned)s, b2_old<M>(smem, d + 3) + 2, SPV,
-                          b2_oldp<M>(smem, d + 3) + 8, wi, 6, err, plan.poll_ns);
+                          b2_oldp<M>(smem, d + 3) + 8, wi, 6, err, plan.poll_ns, plan.jitter);
         if (has_rhs && wi >= 6 && wi < 10 && d + 1 <= dlast)
           band_load<M, 4>(rhsf, plan.ver, b, d + 1, 0, B2W, 0u, smem + (LY::V_RHS + ((d + 1) & 1)) * VEC, SPV,
                           smem + LY::PR + ((d + 1) & 1) * 64, wi - 6, 4, err, 0);
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
                            smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         if (k > 0 && wi == 11 && d + 1 <= dlast)
           band_load<M, 2>(f, plan.ver, b, d, -2, 2, (unsigned)s + 1u, b2_new<M>(smem, d), SPV, b2_newp<M>(smem, d),
-                          0, 1, err, plan.poll_ns);
+                          0, 1, err, plan.poll_ns, plan.jitter);
         if (tid == 128) s_stop = stop_now;
       }
       __syncthreads();

@@ -40,7 +40,7 @@ struct BandPlan {
   int dirs[16];
   unsigned dirbits;  // dirs[s] = (dirbits >> 2s) & 3 (no runtime-indexed param array)
   int poll_ns;
-  int exp;  // experiment flags (debug timing only; results invalid when set)
+  unsigned jitter;  // schedule perturbation seed (race stress tests; 0 = off)
   unsigned long long* trace;  // optional per-task [8] stamps (debug)
   long long trace_cap;
   int nchunks, clen;  // residual mode: diagonal chunks per band and their length
@@ -78,6 +78,16 @@ struct BandGeo {
 // spinning by the waiting CTAs would load the L2 the running tasks use)
 constexpr int kPrologueSleepNs = 512;
 
+// race stress: a pseudo-random 0-2 us sleep of the calling warp (seed != 0)
+__device__ __forceinline__ void sched_jitter(unsigned seed, unsigned site) {
+  if (!seed) return;
+  unsigned h = (unsigned)gtimer() ^ (seed * 0x9e3779b9u) ^ (site * 0x85ebca6bu) ^ (blockIdx.x * 0xc2b2ae35u);
+  h ^= h >> 15;
+  h *= 0x2c1b3c6du;
+  h ^= h >> 12;
+  __nanosleep(h & 2047u);
+}
+
 __device__ __forceinline__ bool band_stop(const DevErr* err) {
   return *((volatile const int*)&err->code) != 0;
 }
@@ -90,7 +100,8 @@ __device__ __forceinline__ bool band_stop(const DevErr* err) {
 template <int M, int MAXS>
 __device__ __forceinline__ void band_load(const DevField& fld, const unsigned* ver, const BandGeo& b, int dd,
                                           int s0, int ns, unsigned need, double* vec, int vstride, double* prm,
-                                          int wi, int nw, DevErr* err, int poll_ns) {
+                                          int wi, int nw, DevErr* err, int poll_ns,
+                                          unsigned jit = 0) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, H = (N + 31) / 32;
   static_assert(MAXS <= 32, "one polling lane per slot");
   constexpr int PR = (4 * MAXS + 31) / 32;  // rounds of parameter loads (4 lanes per slot)
@@ -100,6 +111,7 @@ __device__ __forceinline__ void band_load(const DevField& fld, const unsigned* v
     const int slot = s0 + wi + lane * nw;
     if (slot < s0 + ns) my_cell = b.cell(slot, dd);
   }
+  if (jit && need) sched_jitter(jit, (unsigned)dd);
   if (need && my_cell >= 0) {
     // relaxed polling, one acquire once satisfied (an acquire per poll
     // measured slower: the spinning warps slow the SM's memory pipeline)
@@ -244,6 +256,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
   const unsigned rneed = RES ? 0u : (unsigned)plan.nsweeps;
   for (;;) {
     if (tid == 0) {
+      sched_jitter(plan.jitter, 1u);
       s_task = (int)atomicAdd(plan.next, 1u);
       s_stop = band_stop(err);
     }
@@ -479,6 +492,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         // last CTA barrier, so this release orders it: fence cumulativity; the
         // earlier the publication, the shorter band k+1's halo wait)
         if (g == 1 && q == 0 && d > dfirst && c < BW) {
+          sched_jitter(plan.jitter, (unsigned)d);
           const int cl = b.cell(c, d - 1);
           if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
         }
@@ -534,14 +548,14 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
 
         if (d + 1 <= dlast)
           band_load<M, 5>(f, plan.ver, b, d + 2, 0, NS, res ? rneed : (unsigned)s, smem + LY::V_X * VEC, SPV,
-                          smem + LY::PX, wi, npw, err, plan.poll_ns);
+                          smem + LY::PX, wi, npw, err, plan.poll_ns, plan.jitter);
         if (res && wi == 0 && d + 1 <= dlast)  // (the sweep: group 1 does this)
           band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
                           smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         // band k-1's new cell last: by then it is (nearly always) published
         if (k > 0 && wi == npw - 1 && d + 1 <= dlast)
           band_load<M, 1>(f, plan.ver, b, d, -1, 1, res ? rneed : (unsigned)s + 1u, smem + LY::HALO, 1,
-                          smem + LY::HALOP, 0, 1, err, plan.poll_ns);
+                          smem + LY::HALOP, 0, 1, err, plan.poll_ns, plan.jitter);
         if (wi == 0 && c == 0) {
           s_stop = stop_now;
           if (plan.trace && 4 * task + 3 < plan.trace_cap) s_tr[2] += gtimer() - s_tr[3];

@@ -417,6 +417,7 @@ constexpr bool use_split() { return M <= 5; }
 bool split_sweep_enabled();
 unsigned long long* trace_buffer(long long* cap);
 void poll_tuning(int* split_wait, int* poll_ns);
+unsigned sched_jitter_seed();
 void band_scratch(momg_field* f, unsigned** ver, unsigned** next);
 bool band_sweep_enabled();
 bool band2_enabled();
@@ -491,6 +492,7 @@ struct Launch {
         }
         int sw = 0;
         poll_tuning(&sw, &bp.poll_ns);
+            bp.jitter = sched_jitter_seed();
         const int ndiag = std::min(31, f->nx - 1) + f->ny;
         bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
         bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
@@ -609,7 +611,7 @@ struct Launch {
             }
             int sw = 0;
             poll_tuning(&sw, &bp.poll_ns);
-            bp.exp = sw;
+            bp.jitter = sched_jitter_seed();
             bp.trace = trace_buffer(&bp.trace_cap);
             bp.nchunks = 0;  // no fused residual tasks
             bp.clen = 1;
@@ -621,7 +623,7 @@ struct Launch {
           }
           if (band_sweep_enabled() && band2_enabled()) {
             // second order and/or an FAS rhs: the 16-column band sweep
-            sp::Band2Plan bp;
+            sp::Band2Plan bp{};
             band_scratch(f, &bp.ver, &bp.next);
             bp.nsweeps = 4 * iters;
             bp.nbands = (f->nx + 15) / 16;
@@ -631,6 +633,7 @@ struct Launch {
             bp.has_rhs = rhs != nullptr;
             int sw = 0;
             poll_tuning(&sw, &bp.poll_ns);
+            bp.jitter = sched_jitter_seed();
             if constexpr (M == 3) band2_launch_m3(fd, rd, c, err, bp, momg_rt::stream());
             else if constexpr (M == 4) band2_launch_m4(fd, rd, c, err, bp, momg_rt::stream());
             else band2_launch_m5(fd, rd, c, err, bp, momg_rt::stream());

@@ -537,6 +537,15 @@ void poll_tuning(int* split_wait, int* poll_ns) {
   *poll_ns = ns;
 }
 
+// schedule perturbation for the race stress tests (MOMG_JITTER=<seed>, read
+// at every launch): the band kernels sleep pseudo-random 0-2 us before task
+// claims, publications and polls, so the inter-CTA protocol runs under other
+// interleavings; results must stay bitwise identical
+unsigned sched_jitter_seed() {
+  const char* e = std::getenv("MOMG_JITTER");
+  return e ? (unsigned)std::strtoul(e, nullptr, 10) : 0u;
+}
+
 void band_scratch(momg_field* f, unsigned** ver, unsigned** next) {
   if (!f->sweep_ver) cudaMalloc(&f->sweep_ver, (size_t)f->nx * f->ny * sizeof(unsigned));
   if (!f->band_next) cudaMalloc(&f->band_next, 64);
