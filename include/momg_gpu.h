@@ -180,6 +180,35 @@ int momg_nmg_cycle(const momg_ctx* ctx, momg_field* field, int levels, int s1, i
 int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_opts* opts,
                       momg_report* report, momg_err* err);
 
+/* ---- strip partition: multi-GPU ------------------ */
+/* A level of `grid` split into n <= 8 column strips [bounds[r], bounds[r+1])
+   (widths multiples of 32; nx a multiple of 32).  This process owns strips
+   [first, last]: they are allocated here (momg_strips_field gives each as an
+   ordinary momg_field on its sub-grid, plus its residual field); the other
+   strips belong to peer ranks and are attached with momg_strips_import from
+   the handle their owner exported (CUDA IPC: peer memory over NVLink).  The
+   fused FS iteration + residual then runs this process's band tasks and reads
+   / polls the neighbouring strips' cells in place, so the Gauss-Seidel
+   wavefront (single_level.cpp:121-166) pipelines across strips with no
+   collective.  Ranks must call it in the same sequence, and fields are only
+   written by other entry points while no rank is inside it (the host layer,
+   paper_2206_13164_b200/strips.py, brackets it with barriers).  With all
+   strips owned by one process it is one kernel over every strip (the
+   single-GPU emulation of the ranks). */
+typedef struct momg_strips momg_strips;
+#define MOMG_STRIP_HANDLE_BYTES 320
+int momg_strips_create(const momg_grid* grid, int M, int n, const int* bounds, int first, int last,
+                       momg_strips** out, momg_err* err);
+void momg_strips_destroy(momg_strips* s);
+int momg_strips_field(momg_strips* s, int r, momg_field** field, momg_field** residual);
+int momg_strips_export(momg_strips* s, int r, void* handle /* MOMG_STRIP_HANDLE_BYTES */, momg_err* err);
+int momg_strips_import(momg_strips* s, int r, const void* handle, momg_err* err);
+/* fast_sweep_step (no rhs, first order, M <= 5) + residual into the strips'
+   residual fields, over the partition (nmg_cycle multigrid.cpp:170-176; the
+   C5 step); evals += the owned strips' cell updates */
+int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const int* sweep_order,
+                                    long long* evals, momg_err* err);
+
 /* ---- execution strategy of fast_sweep (same results either way) -------- */
 /* 1 (default): one persistent dataflow kernel per call (band tasks at first
    order, M <= 5; wavefront items otherwise); 3: persistent wavefront items

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
   const int tid = threadIdx.x;
   const int warp = tid >> 5, g = warp / P, q = warp % P, c = tid & 31;
   const int ntasks = plan.nsweeps * plan.nbands;
+  const CellAddr fa{nullptr, f.c, f.p, plan.ver}, ra{nullptr, rhsf.c, rhsf.p, plan.ver};
   const bool has_rhs = plan.has_rhs != 0;
   const bool o2 = plan.order == 2;
   for (;;) {
@@ -192,14 +193,14 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
     // of dfirst-1 and dfirst-2, the rhs of dfirst; then the update scalars
 #pragma unroll 1
     for (int t = 0; t < 3; ++t)
-      band_load<M, 2>(f, plan.ver, b, dfirst + t, 0, 18, (unsigned)s, b2_old<M>(smem, dfirst + t) + 2, SPV,
+      band_load<M, 2>(fa, b, dfirst + t, 0, 18, (unsigned)s, b2_old<M>(smem, dfirst + t) + 2, SPV,
                       b2_oldp<M>(smem, dfirst + t) + 8, warp, 16, err, kPrologueSleepNs);
     if (k > 0 && warp >= 14)
-      band_load<M, 2>(f, plan.ver, b, dfirst - 1 - (warp - 14), -2, 2, (unsigned)s + 1u,
+      band_load<M, 2>(fa, b, dfirst - 1 - (warp - 14), -2, 2, (unsigned)s + 1u,
                       b2_new<M>(smem, dfirst - 1 - (warp - 14)), SPV, b2_newp<M>(smem, dfirst - 1 - (warp - 14)),
                       0, 1, err, kPrologueSleepNs);
     if (has_rhs)
-      band_load<M, 1>(rhsf, plan.ver, b, dfirst, 0, B2W, 0u, smem + (LY::V_RHS + (dfirst & 1)) * VEC, SPV,
+      band_load<M, 1>(ra, b, dfirst, 0, B2W, 0u, smem + (LY::V_RHS + (dfirst & 1)) * VEC, SPV,
                       smem + LY::PR + (dfirst & 1) * 64, warp, 16, err, 0);
     __syncthreads();
     if (warp == 4)
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
     for (int d = dfirst; d <= dlast; ++d) {
       // ---- (A) write-back of step d-1, then the face states of group g
       if (d > dfirst)
-        band_writeback<M>(f, b, d - 1, b2_new<M>(smem, d - 1) + 2, b2_newp<M>(smem, d - 1) + 8, s_ok, warp);
+        band_writeback<M>(fa, b, d - 1, b2_new<M>(smem, d - 1) + 2, b2_newp<M>(smem, d - 1) + 8, s_ok, warp);
       const int jr = d - ir;
       const bool valid = c < B2W && ir < f.nx && jr >= 0 && jr < f.ny;
       const int i = valid ? (b.i_up ? ir : f.nx - 1 - ir) : 0;
@@ -343,23 +344,23 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
           if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
         }
         if (wi < 6 && d + 1 <= dlast)
-          band_load<M, 3>(f, plan.ver, b, d + 3, 0, 18, (unsigned)s, b2_old<M>(smem, d + 3) + 2, SPV,
+          band_load<M, 3>(fa, b, d + 3, 0, 18, (unsigned)s, b2_old<M>(smem, d + 3) + 2, SPV,
                           b2_oldp<M>(smem, d + 3) + 8, wi, 6, err, plan.poll_ns, plan.jitter);
         if (has_rhs && wi >= 6 && wi < 10 && d + 1 <= dlast)
-          band_load<M, 4>(rhsf, plan.ver, b, d + 1, 0, B2W, 0u, smem + (LY::V_RHS + ((d + 1) & 1)) * VEC, SPV,
+          band_load<M, 4>(ra, b, d + 1, 0, B2W, 0u, smem + (LY::V_RHS + ((d + 1) & 1)) * VEC, SPV,
                           smem + LY::PR + ((d + 1) & 1) * 64, wi - 6, 4, err, 0);
         if (wi == 10 && d + 1 <= dlast)
           band_pre<M, B2W>(f, ctx, b, d + 1, b2_old<M>(smem, d + 1) + 2, b2_oldp<M>(smem, d + 1) + 8,
                            smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         if (k > 0 && wi == 11 && d + 1 <= dlast)
-          band_load<M, 2>(f, plan.ver, b, d, -2, 2, (unsigned)s + 1u, b2_new<M>(smem, d), SPV, b2_newp<M>(smem, d),
+          band_load<M, 2>(fa, b, d, -2, 2, (unsigned)s + 1u, b2_new<M>(smem, d), SPV, b2_newp<M>(smem, d),
                           0, 1, err, plan.poll_ns, plan.jitter);
         if (tid == 128) s_stop = stop_now;
       }
       __syncthreads();
       if (s_stop) return;
     }
-    band_writeback<M>(f, b, dlast, b2_new<M>(smem, dlast) + 2, b2_newp<M>(smem, dlast) + 8, s_ok, warp);
+    band_writeback<M>(fa, b, dlast, b2_new<M>(smem, dlast) + 2, b2_newp<M>(smem, dlast) + 8, s_ok, warp);
     __syncthreads();
     if (warp == 4 && c < B2W) {
       const int cl = b.cell(c, dlast);

@@ -28,9 +28,39 @@
 #pragma once
 
 #include "split_cell.cuh"
+#include "strips.h"
 
 namespace momg_gpu {
 namespace sp {
+
+// Global addresses of a cell handle (flat field, or strip table)
+struct CellAddr {
+  const StripTab* st;
+  double* c;
+  double* p;
+  unsigned* ver;
+  __device__ __forceinline__ double* cptr(int h, int NP) const {
+    return st ? (double*)__ldg((const unsigned long long*)&st->c[h >> kStripShift]) + (size_t)(h & kStripMask) * NP
+              : c + (size_t)h * NP;
+  }
+  __device__ __forceinline__ double* pptr(int h) const {
+    return st ? (double*)__ldg((const unsigned long long*)&st->p[h >> kStripShift]) + (size_t)(h & kStripMask) * 4
+              : p + (size_t)h * 4;
+  }
+  __device__ __forceinline__ unsigned* vptr(int h) const {
+    return st ? (unsigned*)__ldg((const unsigned long long*)&st->ver[h >> kStripShift]) + (h & kStripMask)
+              : ver + h;
+  }
+  __device__ __forceinline__ double* ocptr(int h, int NP, double* flat) const {
+    return st ? (double*)__ldg((const unsigned long long*)&st->oc[h >> kStripShift]) +
+                    (size_t)(h & kStripMask) * NP
+              : flat + (size_t)h * NP;
+  }
+  __device__ __forceinline__ double* opptr(int h, double* flat) const {
+    return st ? (double*)__ldg((const unsigned long long*)&st->op[h >> kStripShift]) + (size_t)(h & kStripMask) * 4
+              : flat + (size_t)h * 4;
+  }
+};
 
 struct BandPlan {
   unsigned* ver;       // per-cell sweep counters (zeroed per launch)
@@ -44,6 +74,15 @@ struct BandPlan {
   unsigned long long* trace;  // optional per-task [8] stamps (debug)
   long long trace_cap;
   int nchunks, clen;  // residual mode: diagonal chunks per band and their length
+  // strips (nullptr: one flat field).  A launch runs the tasks of the rotated
+  // bands [kb, kb + nk) of every sweep, kb = kb_up for i-ascending sweeps and
+  // kb_dn for i-descending ones (a rank's own strips); the counters then count
+  // from `epoch` (need = epoch + s) and are never reset, and `sys` selects
+  // system-scope polls / releases (strips on peer GPUs)
+  const StripTab* strips;
+  unsigned epoch;
+  int kb_up, kb_dn, nk;
+  int sys;
 };
 
 template <int M>
@@ -65,12 +104,18 @@ struct BandLayout {
 struct BandGeo {
   int nx, ny, k, bw;
   bool i_up, j_up;
-  // rotated cell (ir = 32k + slot, jr = dd - ir) -> flat index, or -1
+  const StripTab* st = nullptr;
+  // rotated cell (ir = 32k + slot, jr = dd - ir) -> cell handle, or -1
   __device__ __forceinline__ int cell(int slot, int dd) const {
     const int ir = bw * k + slot, jr = dd - ir;
     if (ir < 0 || ir >= nx || jr < 0 || jr >= ny) return -1;
     const int i = i_up ? ir : nx - 1 - ir, j = j_up ? jr : ny - 1 - jr;
-    return j * nx + i;
+    if (!st) return j * nx + i;
+    const int n = __ldg(&st->n);
+    int r = 0;
+    for (int t = 1; t < n; ++t) r += i >= __ldg(&st->i0[t]) ? 1 : 0;
+    const int i0 = __ldg(&st->i0[r]), w = __ldg(&st->i0[r + 1]) - i0;
+    return (r << kStripShift) | (j * w + i - i0);
   }
 };
 
@@ -98,10 +143,9 @@ __device__ __forceinline__ bool band_stop(const DevErr* err) {
 // `need` (0: no wait).  All of a warp's polls, then all of its loads, are in
 // flight together.
 template <int M, int MAXS>
-__device__ __forceinline__ void band_load(const DevField& fld, const unsigned* ver, const BandGeo& b, int dd,
-                                          int s0, int ns, unsigned need, double* vec, int vstride, double* prm,
-                                          int wi, int nw, DevErr* err, int poll_ns,
-                                          unsigned jit = 0) {
+__device__ __forceinline__ void band_load(const CellAddr& fld, const BandGeo& b, int dd, int s0, int ns,
+                                          unsigned need, double* vec, int vstride, double* prm, int wi, int nw,
+                                          DevErr* err, int poll_ns, unsigned jit = 0, bool sys = false) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, H = (N + 31) / 32;
   static_assert(MAXS <= 32, "one polling lane per slot");
   constexpr int PR = (4 * MAXS + 31) / 32;  // rounds of parameter loads (4 lanes per slot)
@@ -115,9 +159,9 @@ __device__ __forceinline__ void band_load(const DevField& fld, const unsigned* v
   if (need && my_cell >= 0) {
     // relaxed polling, one acquire once satisfied (an acquire per poll
     // measured slower: the spinning warps slow the SM's memory pipeline)
-    const unsigned* a = ver + my_cell;
+    const unsigned* a = fld.vptr(my_cell);
     long long polls = 0;
-    while (ld_relaxed(a) < need) {
+    while (ld_relaxed_s(a, sys) < need) {
       if (band_stop(err)) break;
       if (++polls > (1LL << 26)) {
         tc::raise(err, E_ERROR, W_DEADLOCK, my_cell % b.nx, my_cell / b.nx, (double)need);
@@ -125,7 +169,7 @@ __device__ __forceinline__ void band_load(const DevField& fld, const unsigned* v
       }
       if (poll_ns) __nanosleep(poll_ns);
     }
-    (void)ld_acquire(a);
+    (void)ld_acquire_s(a, sys);
   }
   __syncwarp();
   double r[MAXS][H];
@@ -136,14 +180,14 @@ __device__ __forceinline__ void band_load(const DevField& fld, const unsigned* v
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const int kk = lane + 32 * h;
-      r[t][h] = (cl >= 0 && kk < N) ? __ldcg(fld.c + (size_t)cl * NP + kk) : 0.0;
+      r[t][h] = (cl >= 0 && kk < N) ? __ldcg(fld.cptr(cl, NP) + kk) : 0.0;
     }
   }
 #pragma unroll
   for (int rr = 0; rr < PR; ++rr) {
     const int t = (lane + 32 * rr) >> 2;
     const int cl = __shfl_sync(0xffffffffu, my_cell, t < MAXS ? t : 0);
-    pr[rr] = (t < MAXS && cl >= 0) ? __ldcg(fld.p + (size_t)cl * 4 + (lane & 3)) : 0.0;
+    pr[rr] = (t < MAXS && cl >= 0) ? __ldcg(fld.pptr(cl) + (lane & 3)) : 0.0;
   }
 #pragma unroll
   for (int t = 0; t < MAXS; ++t) {
@@ -201,7 +245,7 @@ __device__ __forceinline__ void band_pre(const DevField& f, const DevCtx& ctx, c
 // coefficient (coalesced).  Runs at the start of the next step on all warps,
 // so the update's critical path ends with its last projection pass.
 template <int M>
-__device__ __forceinline__ void band_writeback(const DevField& f, const BandGeo& b, int dd, const double* V,
+__device__ __forceinline__ void band_writeback(const CellAddr& f, const BandGeo& b, int dd, const double* V,
                                                const double* PV, const int* ok, int warp) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3;
   const int lane = threadIdx.x & 31;
@@ -210,7 +254,7 @@ __device__ __forceinline__ void band_writeback(const DevField& f, const BandGeo&
     const int cc = 2 * warp + t;
     const int cl = ok[cc] ? b.cell(cc, dd) : -1;
     if (cl < 0) continue;
-    double* dst = f.c + (size_t)cl * NP;
+    double* dst = f.cptr(cl, NP);
     double r[(N + 31) / 32];
 #pragma unroll
     for (int h = 0; h < (N + 31) / 32; ++h) {
@@ -222,7 +266,7 @@ __device__ __forceinline__ void band_writeback(const DevField& f, const BandGeo&
       const int k = lane + 32 * h;
       if (k < N) __stcg(dst + k, r[h]);
     }
-    if (lane < 4) __stcg(f.p + (size_t)cl * 4 + lane, PV[cc * 4 + lane]);
+    if (lane < 4) __stcg(f.pptr(cl) + lane, PV[cc * 4 + lane]);
   }
 }
 
@@ -251,9 +295,12 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
   // sweep tasks (sweep, band), then residual tasks (chunk, band): the
   // standalone residual (RES) has only the latter; a fused sweep+residual
   // launch (plan.nchunks > 0) appends them, polling for the final version
-  const int sweep_tasks = RES ? 0 : plan.nsweeps * plan.nbands;
-  const int ntasks = sweep_tasks + plan.nchunks * plan.nbands;
-  const unsigned rneed = RES ? 0u : (unsigned)plan.nsweeps;
+  const int sweep_tasks = RES ? 0 : plan.nsweeps * plan.nk;
+  const int ntasks = sweep_tasks + plan.nchunks * plan.nk;
+  const unsigned ep = plan.epoch;  // counters count from here (0: zeroed per launch)
+  const unsigned rneed = RES ? 0u : ep + (unsigned)plan.nsweeps;
+  const bool sys = plan.sys != 0;
+  const CellAddr fa{plan.strips, f.c, f.p, plan.ver};
   for (;;) {
     if (tid == 0) {
       sched_jitter(plan.jitter, 1u);
@@ -265,9 +312,10 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     if (task >= ntasks || s_stop) return;
     const bool res = task >= sweep_tasks;  // uniform per task
     const int rtask = task - sweep_tasks;
-    const int s = res ? plan.nsweeps - 1 : task / plan.nbands, k = (res ? rtask : task) % plan.nbands;
+    const int s = res ? plan.nsweeps - 1 : task / plan.nk;
     // residual tasks walk the frame of the last sweep, whose wavefront they follow
     const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
+    const int k = (dir == 0 || dir == 3 ? plan.kb_up : plan.kb_dn) + (res ? rtask : task) % plan.nk;
     BandGeo b;
     b.nx = f.nx;
     b.ny = f.ny;
@@ -275,10 +323,11 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     b.bw = BW;
     b.i_up = dir == 0 || dir == 3;  // kSweepDirs (single_level.cpp:116-117)
     b.j_up = dir == 0 || dir == 1;
+    b.st = plan.strips;
     const int ir = BW * k + c;
     int dfirst = BW * k, dlast = min(BW * k + BW - 1, f.nx - 1) + f.ny - 1;
     if (res) {
-      dfirst += (rtask / plan.nbands) * plan.clen;
+      dfirst += (rtask / plan.nk) * plan.clen;
       dlast = min(dlast, dfirst + plan.clen - 1);
       if (dfirst > dlast) {  // empty chunk of a partial band
         __syncthreads();
@@ -297,10 +346,11 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     if (!res && warp == 0) {
       for (int e = c; e < 2 * NS + 1; e += 32) {
         const int cl = e < 2 * NS ? b.cell(e % NS, dfirst + e / NS) : (k > 0 ? b.cell(-1, dfirst - 1) : -1);
-        const unsigned need = e < 2 * NS ? (unsigned)s : (unsigned)s + 1u;
+        const unsigned need = ep + (e < 2 * NS ? (unsigned)s : (unsigned)s + 1u);
         if (cl >= 0 && need) {
           long long polls = 0;
-          while (ld_relaxed(plan.ver + cl) < need) {
+          const unsigned* a = fa.vptr(cl);
+          while (ld_relaxed_s(a, sys) < need) {
             if (band_stop(err)) break;
             if (++polls > (1LL << 26)) {
               tc::raise(err, E_ERROR, W_DEADLOCK, cl % f.nx, cl / f.nx, (double)need);
@@ -308,21 +358,21 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
             }
             __nanosleep(kPrologueSleepNs);
           }
-          (void)ld_acquire(plan.ver + cl);
+          (void)ld_acquire_s(a, sys);
         }
       }
     }
     __syncthreads();
     const unsigned pn = res ? rneed : 0u;  // sweep tasks polled above
-    band_load<M, 4>(f, plan.ver, b, dfirst, 0, NS, pn, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp, 16, err,
+    band_load<M, 4>(fa, b, dfirst, 0, NS, pn, smem + LY::V_OLD1 * VEC, SPV, smem + LY::PO, warp, 16, err,
                     kPrologueSleepNs);
-    band_load<M, 4>(f, plan.ver, b, dfirst + 1, 0, NS, pn, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err,
+    band_load<M, 4>(fa, b, dfirst + 1, 0, NS, pn, smem + LY::V_X * VEC, SPV, smem + LY::PX, warp, 16, err,
                     kPrologueSleepNs);
     if (k > 0 && warp == 15)
-      band_load<M, 1>(f, plan.ver, b, dfirst - 1, -1, 1, pn, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1, err,
+      band_load<M, 1>(fa, b, dfirst - 1, -1, 1, pn, smem + LY::HALO, 1, smem + LY::HALOP, 0, 1, err,
                       kPrologueSleepNs);
     if (res)  // a chunk may start mid-band: its upstream states are old(dfirst-1)
-      band_load<M, 2>(f, plan.ver, b, dfirst - 1, 0, BW, pn, smem + LY::V_V * VEC, SPV, smem + LY::PV, warp, 16,
+      band_load<M, 2>(fa, b, dfirst - 1, 0, BW, pn, smem + LY::V_V * VEC, SPV, smem + LY::PV, warp, 16,
                       err, kPrologueSleepNs);
     __syncthreads();
     if (warp == 4)
@@ -335,7 +385,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     for (int d = dfirst; d <= dlast; ++d) {
       if (tr) s_tr[3] = gtimer();
       // write-back of step d-1 (V is read here before (A) overwrites it)
-      if (!res && d > dfirst) band_writeback<M>(f, b, d - 1, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
+      if (!res && d > dfirst) band_writeback<M>(fa, b, d - 1, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
       // ---- (A) stage the step's face states.  Sources: OLD1 (own old
       // states), X (old states of diagonal d+1), V (= L of group 1: new
       // states of d-1) and HALO.  Every destination except group 1's L is
@@ -461,19 +511,20 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         {  // coalesced store of R: warp q stores cells 8q..8q+7, lane = coefficient
           constexpr int NP = (N + 3) & ~3;
           const bool ok = valid && w == W_NONE;
-          const size_t cell = (size_t)j * f.nx + i;
+          const int cell = valid ? b.cell(c, d) : 0;
           if (ok && q == 0) {
-            __stcg(reinterpret_cast<double2*>(out.p + cell * 4), make_double2(cp.v[0], cp.v[1]));
-            __stcg(reinterpret_cast<double2*>(out.p + cell * 4) + 1, make_double2(cp.v[2], cp.v[3]));
+            double* op = fa.opptr(cell, out.p);
+            __stcg(reinterpret_cast<double2*>(op), make_double2(cp.v[0], cp.v[1]));
+            __stcg(reinterpret_cast<double2*>(op) + 1, make_double2(cp.v[2], cp.v[3]));
           }
           const double* Db = D - c;
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
             const int cc = 8 * q + t;
             const int okc = __shfl_sync(0xffffffffu, ok ? 1 : 0, cc);
-            const long long bc = __shfl_sync(0xffffffffu, (long long)cell, cc);
+            const int bc = __shfl_sync(0xffffffffu, cell, cc);
             if (!okc) continue;
-            double* dst = out.c + (size_t)bc * NP;
+            double* dst = fa.ocptr(bc, NP, out.c);
 #pragma unroll
             for (int h = 0; h < (N + 31) / 32; ++h) {
               const int kq = c + 32 * h;
@@ -494,7 +545,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         if (g == 1 && q == 0 && d > dfirst && c < BW) {
           sched_jitter(plan.jitter, (unsigned)d);
           const int cl = b.cell(c, d - 1);
-          if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
+          if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, sys);
         }
         {
           const double* pre = smem + LY::PRE + (d & 1) * PRE_N * 32 + c;
@@ -547,15 +598,15 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         // update's critical path carries no memory fence
 
         if (d + 1 <= dlast)
-          band_load<M, 5>(f, plan.ver, b, d + 2, 0, NS, res ? rneed : (unsigned)s, smem + LY::V_X * VEC, SPV,
-                          smem + LY::PX, wi, npw, err, plan.poll_ns, plan.jitter);
+          band_load<M, 5>(fa, b, d + 2, 0, NS, res ? rneed : ep + (unsigned)s, smem + LY::V_X * VEC, SPV,
+                          smem + LY::PX, wi, npw, err, plan.poll_ns, plan.jitter, sys);
         if (res && wi == 0 && d + 1 <= dlast)  // (the sweep: group 1 does this)
           band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
                           smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         // band k-1's new cell last: by then it is (nearly always) published
         if (k > 0 && wi == npw - 1 && d + 1 <= dlast)
-          band_load<M, 1>(f, plan.ver, b, d, -1, 1, res ? rneed : (unsigned)s + 1u, smem + LY::HALO, 1,
-                          smem + LY::HALOP, 0, 1, err, plan.poll_ns, plan.jitter);
+          band_load<M, 1>(fa, b, d, -1, 1, res ? rneed : ep + (unsigned)s + 1u, smem + LY::HALO, 1,
+                          smem + LY::HALOP, 0, 1, err, plan.poll_ns, plan.jitter, sys);
         if (wi == 0 && c == 0) {
           s_stop = stop_now;
           if (plan.trace && 4 * task + 3 < plan.trace_cap) s_tr[2] += gtimer() - s_tr[3];
@@ -566,11 +617,11 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
       if (tr) s_tr[6] += gtimer() - s_tr[3];
       if (s_stop) return;
     }
-    if (!res) band_writeback<M>(f, b, dlast, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
+    if (!res) band_writeback<M>(fa, b, dlast, smem + LY::V_V * VEC, smem + LY::PV, s_ok, warp);
     __syncthreads();
     if (!res && warp == 4 && c < BW) {  // publish the last step
       const int cl = b.cell(c, dlast);
-      if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
+      if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, sys);
     }
     if (tr) {
       unsigned long long* o = plan.trace + (size_t)task * 32;

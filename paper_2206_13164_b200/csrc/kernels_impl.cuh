@@ -485,6 +485,7 @@ struct Launch {
         band_scratch(f, &bp.ver, &bp.next);
         bp.nsweeps = 4 * iters;
         bp.nbands = (f->nx + 31) / 32;
+        bp.nk = bp.nbands;
         bp.dirbits = 0;
         for (int s = 0; s < 16; ++s) {
           bp.dirs[s] = order[s & 3];
@@ -527,6 +528,7 @@ struct Launch {
         band_scratch(out, &bp.ver, &bp.next);
         bp.nsweeps = 1;
         bp.nbands = (f->nx + 31) / 32;
+        bp.nk = bp.nbands;
         const int ndiag = std::min(31, f->nx - 1) + f->ny;
         bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
         bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
@@ -600,10 +602,11 @@ struct Launch {
               battr = true;
             }
             const int bw = 32;  // columns per band task (16 measured no faster per step: latency-bound)
-            sp::BandPlan bp;
+            sp::BandPlan bp{};
             band_scratch(f, &bp.ver, &bp.next);
             bp.nsweeps = 4 * iters;
             bp.nbands = (f->nx + bw - 1) / bw;
+            bp.nk = bp.nbands;
             bp.dirbits = 0;
             for (int s = 0; s < 16; ++s) {
               bp.dirs[s] = order[s & 3];
@@ -802,9 +805,57 @@ struct Launch {
     k_norm_partial<M><<<blocks, 256, 0, momg_rt::stream()>>>(res->dev(), field->dev(), partial);
     momg_rt::count_launch(1);
   }
+  // the fused FS iteration + residual over a strip partition (one launch for
+  // this process's strips; first order, M <= 5)
+  static bool strips_sweep_res(const DevCtx& ctx, const StripLaunch& L) {
+    if constexpr (use_split<M>()) {
+      if (ctx.order != 1) return false;
+      static bool battr = false;
+      if (!battr) {
+        set_smem(sp::k5_band<M, 32>, sp::BandLayout<M>::bytes);
+        battr = true;
+      }
+      sp::BandPlan bp{};
+      bp.next = L.next;
+      bp.nsweeps = 4;
+      bp.nbands = L.nbands;
+      bp.dirbits = 0;
+      for (int s = 0; s < 16; ++s) {
+        bp.dirs[s] = L.order[s & 3];
+        bp.dirbits |= (unsigned)(L.order[s & 3] & 3) << (2 * s);
+      }
+      int sw = 0;
+      poll_tuning(&sw, &bp.poll_ns);
+      bp.jitter = sched_jitter_seed();
+      const int ndiag = std::min(31, L.geo.nx - 1) + L.geo.ny;
+      bp.nchunks = std::max(1, (2 * 148 + L.nk - 1) / L.nk);
+      bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
+      bp.nchunks = (ndiag + bp.clen - 1) / bp.clen;
+      bp.strips = (const sp::StripTab*)L.tab;
+      bp.epoch = L.epoch;
+      bp.kb_up = L.kb_up;
+      bp.kb_dn = L.kb_dn;
+      bp.nk = L.nk;
+      bp.sys = L.sys;
+      int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
+      const int tasks = (bp.nsweeps + bp.nchunks) * bp.nk;
+      if (nb > tasks) nb = tasks;
+      DevCtx c = ctx;
+      DevField none = L.geo;
+      none.c = none.p = nullptr;
+      sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(
+          L.geo, c, momg_rt::err_dev(), bp, none);
+      momg_rt::note_launch(cudaGetLastError());
+      momg_rt::count_launch(1);
+      return true;
+    }
+    (void)ctx;
+    (void)L;
+    return false;
+  }
   static const Ops* ops() {
     static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial, sweep_n, sweep_res,
-                          euler};
+                          euler, strips_sweep_res};
     return &o;
   }
 };

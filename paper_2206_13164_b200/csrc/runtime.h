@@ -60,6 +60,16 @@ void acquire(const momg_field* f);
 }  // namespace momg_rt
 
 namespace momg_gpu {
+// One fused FS + residual launch over a strip-partitioned level (runtime.cu
+// momg_strips_*; the table is a device-resident sp::StripTab)
+struct StripLaunch {
+  DevField geo;       // global nx, ny, dx, dy (c, p unused)
+  const void* tab;    // device sp::StripTab
+  unsigned* next;     // task counter of this process (zeroed by the caller)
+  unsigned epoch;     // counters count from here
+  int nbands, kb_up, kb_dn, nk, sys;
+  int order[4];
+};
 // Per-moment-order launchers (kernels_m<M>.cu).
 struct Ops {
   void (*residual)(const DevCtx&, const momg_field*, momg_field*);
@@ -72,6 +82,7 @@ struct Ops {
   void (*sweep_n)(const DevCtx&, momg_field*, const momg_field*, const int*, int);
   bool (*sweep_res)(const DevCtx&, momg_field*, const int*, momg_field*, int);
   void (*euler)(const momg_field*, const momg_field*, const momg_field*, const double*);
+  bool (*strips_sweep_res)(const DevCtx&, const StripLaunch&);
 };
 const Ops* ops_for(int M);
 DevCtx make_ctx(const momg_ctx* c);

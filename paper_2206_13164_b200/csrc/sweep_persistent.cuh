@@ -49,6 +49,31 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// system scope: counters and cells shared with peer GPUs over NVLink (row
+// strips on several ranks; peer-mapped memory)
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_s(const unsigned* p, bool sys) {
+  return sys ? ld_relaxed_sys(p) : ld_relaxed(p);
+}
+__device__ __forceinline__ unsigned ld_acquire_s(const unsigned* p, bool sys) {
+  return sys ? ld_acquire_sys(p) : ld_acquire(p);
+}
+__device__ __forceinline__ void st_release_s(unsigned* p, unsigned v, bool sys) {
+  if (sys) st_release_sys(p, v);
+  else st_release(p, v);
+}
 
 struct SweepPlan {
   const uint32_t* order;  // diagonal-major (ii | jj << 16) for direction (i+, j+)

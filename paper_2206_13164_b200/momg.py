@@ -325,9 +325,19 @@ class CellField:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib is not None:
+        if h is not None and h.value and _lib is not None and getattr(self, "_owned", True):
             _lib.momg_field_destroy(h)
             self._h = None
+
+    @classmethod
+    def _view(cls, grid: Grid2D, order: int, handle: int, keep) -> "CellField":
+        """A field owned by another object (a strip of a StripSet)."""
+        f = cls.__new__(cls)
+        f.grid, f.order, f.N = grid, order, count(order)
+        f._h = C.c_void_p(handle)
+        f._owned = False
+        f._keep = keep
+        return f
 
     @property
     def handle(self):
@@ -501,6 +511,101 @@ def solve_steady(field: CellField, ctx: SolveContext, options: SolverOptions,
         raise NonConvergence(err.msg.decode(errors="replace"), report)
     _raise(rc, err)
     return report
+
+
+# ------------------------------------------------------------------ strips
+STRIP_HANDLE_BYTES = 320
+
+
+def strip_grid(grid: Grid2D, i0: int, i1: int) -> Grid2D:
+    """The sub-grid of columns [i0, i1) (a strip's own level)."""
+    dx = np.ascontiguousarray(grid.dx[i0:i1], dtype=np.float64)
+    return Grid2D(i1 - i0, grid.ny, float(np.sum(dx)), grid.Ly, dx, np.array(grid.dy, dtype=np.float64),
+                  np.ascontiguousarray(grid.xc[i0:i1], dtype=np.float64), np.array(grid.yc, dtype=np.float64))
+
+
+class StripSet:
+    """momg_strips (include/momg_gpu.h): a level split into column strips
+    [bounds[r], bounds[r+1]); this process owns strips first..last (device
+    fields here), the others are attached from their owners' handles (CUDA
+    IPC, peer memory).  fast_sweep_residual runs the owned strips' band tasks
+    of the fused FS iteration + residual; with every strip owned it is the
+    one-GPU emulation of all ranks in one kernel."""
+
+    def __init__(self, grid: Grid2D, order: int, bounds, first: int = 0, last: int | None = None):
+        self.grid, self.order = grid, order
+        self.bounds = [int(b) for b in bounds]
+        self.n = len(self.bounds) - 1
+        self.first, self.last = first, (self.n - 1 if last is None else last)
+        b = (C.c_int * (self.n + 1))(*self.bounds)
+        h = C.c_void_p()
+        err = _Err()
+        g = grid._c()
+        _raise(lib().momg_strips_create(C.byref(g), order, self.n, b, self.first, self.last, C.byref(h),
+                                        C.byref(err)), err)
+        self._h = h
+        self._fields = {}
+        for r in range(self.first, self.last + 1):
+            fh, rh = C.c_void_p(), C.c_void_p()
+            if lib().momg_strips_field(self._h, r, C.byref(fh), C.byref(rh)):
+                raise Error("momg_strips_field failed")
+            sg = strip_grid(grid, self.bounds[r], self.bounds[r + 1])
+            self._fields[r] = (CellField._view(sg, order, fh.value, self), CellField._view(sg, order, rh.value, self))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.momg_strips_destroy(h)
+            self._h = None
+
+    def field(self, r: int) -> CellField:
+        return self._fields[r][0]
+
+    def residual_field(self, r: int) -> CellField:
+        return self._fields[r][1]
+
+    def export(self, r: int) -> bytes:
+        buf = (C.c_char * STRIP_HANDLE_BYTES)()
+        err = _Err()
+        _raise(lib().momg_strips_export(self._h, r, buf, C.byref(err)), err)
+        return bytes(buf)
+
+    def attach(self, r: int, handle: bytes) -> None:
+        buf = (C.c_char * STRIP_HANDLE_BYTES).from_buffer_copy(handle)
+        err = _Err()
+        _raise(lib().momg_strips_import(self._h, r, buf, C.byref(err)), err)
+
+    def upload(self, coeffs: np.ndarray, params: np.ndarray) -> None:
+        """Owned strips' columns of a global host field (reference order)."""
+        n = count(self.order)
+        c = np.asarray(coeffs).reshape(self.grid.ny, self.grid.nx, n)
+        p = np.asarray(params).reshape(self.grid.ny, self.grid.nx, 4)
+        for r, (f, _) in self._fields.items():
+            i0, i1 = self.bounds[r], self.bounds[r + 1]
+            f.upload(c[:, i0:i1].reshape(-1, n), p[:, i0:i1].reshape(-1, 4))
+
+    def download(self, residual: bool = False):
+        """Owned strips' columns assembled into global-layout arrays (other
+        columns NaN)."""
+        n = count(self.order)
+        c = np.full((self.grid.ny, self.grid.nx, n), np.nan)
+        p = np.full((self.grid.ny, self.grid.nx, 4), np.nan)
+        for r, pair in self._fields.items():
+            i0, i1 = self.bounds[r], self.bounds[r + 1]
+            sc, sp = pair[1 if residual else 0].download()
+            c[:, i0:i1] = sc.reshape(self.grid.ny, i1 - i0, n)
+            p[:, i0:i1] = sp.reshape(self.grid.ny, i1 - i0, 4)
+        return c.reshape(-1, n), p.reshape(-1, 4)
+
+    def fast_sweep_residual(self, ctx: SolveContext, sweep_order=(0, 1, 2, 3), work: WorkStats | None = None):
+        err = _Err()
+        c = ctx._c(self.order)
+        ev = C.c_longlong(0)
+        order = (C.c_int * 4)(*sweep_order)
+        rc = lib().momg_strips_fast_sweep_residual(C.byref(c), self._h, order, C.byref(ev), C.byref(err))
+        if work is not None:
+            work.cell_evals += ev.value
+        _raise(rc, err)
 
 
 def synchronize() -> None:
