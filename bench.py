@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=128)
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--strips", type=int, default=0,
+                    help="world 1: run the strip-partitioned path with this many strips in one process "
+                         "(the one-GPU emulation of the ranks); world > 1 always runs one strip per rank")
     return ap.parse_args()
 
 
@@ -507,10 +510,155 @@ def nmg_cpu_c2(iterations, cycles=1):
                     f"host, extrapolated to {iterations} iterations (labelled extrapolated)"}
 
 
+def strips_arm(a):
+    """C5 strong-scaling step on N GPUs (torchrun, one process per GPU): the
+    2048^2 field split into N column strips (one per rank, peer-mapped over
+    NVLink), the fused FS iteration + residual as one band launch per rank that
+    pipelines the wavefront across strips (momg_strips_fast_sweep_residual),
+    then the strip-local restrict/prolong pair.  With world 1 and --strips K it
+    runs the K-strip partition in one process (all ranks in one kernel)."""
+    import torch
+
+    from paper_2206_13164_b200 import momg
+    from paper_2206_13164_b200.strips import StripComm, StripLevel
+    from paper_2206_13164_b200.synthetic import c5_field
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    err = momg._Err()
+    momg.lib().momg_init(local, momg.C.byref(err))
+    momg.lib().momg_set_stream(momg.C.c_void_p(stream.cuda_stream))
+    comm = StripComm(dist, device=torch.device("cuda", local))
+    nx, M = a.nx, a.M
+    N = momg.count(M)
+    g = momg.Grid2D.uniform(nx, nx)
+    ctx = momg.cavity_context(M, a.order, knudsen=0.1, lid=0.0)
+    c_host, p_host = c5_field(nx, nx, M, seed=a.seed)  # one global field, every rank uploads its columns
+    level = StripLevel(momg, g, M, comm, emulate_ranks=a.strips or None)
+    level.upload(c_host, p_host)
+    per = {}
+    for r in level.owned:
+        f = level.field(r)
+        cg = momg.Grid2D(f.grid.nx // 2, f.grid.ny // 2, f.grid.Lx, f.grid.Ly, *_coarse_arrays(f.grid))
+        dc, _ = c5_field(cg.nx, cg.ny, M, seed=a.seed + 99 + r)
+        dc[:, :10] = 0.0
+        dc *= 1e-3
+        per[r] = dict(coarse=momg.CellField(cg, M), before=momg.CellField(cg, M), after=momg.CellField(cg, M),
+                      crhs=momg.CellField(cg, M),
+                      delta=momg.CellField.from_host(cg, M, dc, np.zeros((cg.cells(), 4))))
+    L, E, C = momg.lib(), momg._Err, momg.C
+
+    def ck(rc, e):
+        if rc:
+            raise RuntimeError(f"momg rc {rc}: {e.msg.decode(errors='replace')}")
+
+    def step(evs=None):
+        e = E()
+        if evs:
+            evs[0].record(stream)
+        level.sweep_residual(ctx)
+        if evs:
+            evs[1].record(stream)
+        for r, b in per.items():
+            f, res = level.field(r), level.residual_field(r)
+            ck(L.momg_restrict_solution(f.handle, b["coarse"].handle, C.byref(e)), e)
+            ck(L.momg_field_copy(b["before"].handle, b["coarse"].handle, C.byref(e)), e)
+            ck(L.momg_defect(res.handle, None, res.handle, C.byref(e)), e)
+            ck(L.momg_restrict_residual(res.handle, b["coarse"].handle, b["crhs"].handle, C.byref(e)), e)
+            ck(L.momg_field_copy(b["after"].handle, b["coarse"].handle, C.byref(e)), e)
+            ck(L.momg_axpy(b["after"].handle, b["delta"].handle, C.byref(e)), e)
+            ck(L.momg_fas_correct(f.handle, b["before"].handle, b["after"].handle, C.byref(e)), e)
+        if evs:
+            evs[2].record(stream)
+
+    for _ in range(a.warmup):
+        step()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(a.steps)]
+    launches0 = momg.launch_count()
+    with Clocks(local) as clk:
+        comm.fence(torch.cuda.synchronize)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for s_ in range(a.steps):
+            step(evs[s_])
+        t1.record(stream)
+        comm.fence(torch.cuda.synchronize)
+    launches = momg.launch_count() - launches0
+    ms_step = comm.allreduce_max(t0.elapsed_time(t1)) / a.steps
+    sweep_med = statistics.median([e[0].elapsed_time(e[1]) for e in evs])
+    xfer_med = statistics.median([e[1].elapsed_time(e[2]) for e in evs])
+    updates = 4.0 * nx * nx
+    value = updates / (ms_step * 1e-3)
+    # end to end: every rank uploads its strip's columns from pinned host
+    # memory, runs the step and downloads its strip, all inside the timed region
+    e2e = None
+    if not a.no_e2e:
+        pin = lambda *shape: torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()  # noqa: E731
+        host = {}
+        for r in level.owned:
+            i0, i1 = level.bounds[r], level.bounds[r + 1]
+            hc = pin(nx * (i1 - i0), N)
+            hp = pin(nx * (i1 - i0), 4)
+            hc[:] = c_host.reshape(nx, nx, N)[:, i0:i1].reshape(-1, N)
+            hp[:] = p_host.reshape(nx, nx, 4)[:, i0:i1].reshape(-1, 4)
+            host[r] = (hc, hp, pin(nx * (i1 - i0), N), pin(nx * (i1 - i0), 4))
+        comm.fence(torch.cuda.synchronize)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e = E()
+        e0.record(stream)
+        for _ in range(a.steps):
+            for r, (hc, hp, oc, op) in host.items():
+                ck(L.momg_field_upload_overlapped(level.field(r).handle, momg._dp(hc), momg._dp(hp), C.byref(e)), e)
+            step()
+            for r, (hc, hp, oc, op) in host.items():
+                ck(L.momg_field_download_overlapped(level.field(r).handle, momg._dp(oc), momg._dp(op),
+                                                    C.byref(e)), e)
+        ck(L.momg_copy_barrier(C.byref(e)), e)
+        e1.record(stream)
+        comm.fence(torch.cuda.synchronize)
+        ck(L.momg_synchronize(C.byref(e)), e)
+        e2e_ms = comm.allreduce_max(e0.elapsed_time(e1) / a.steps)
+        hb = sum(h[0].nbytes + h[1].nbytes for h in host.values())
+        db = sum(h[2].nbytes + h[3].nbytes for h in host.values())
+        e2e = {"value": updates / (e2e_ms * 1e-3), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": int(comm.allreduce_sum(hb)), "d2h_bytes_per_step": int(comm.allreduce_sum(db)),
+               "ms_per_step": e2e_ms,
+               "mode": "each rank uploads its strip (pinned host), runs the step, downloads its strip"}
+    if rank == 0:
+        nstrips = len(level.bounds) - 1
+        line = {"metric": "smoother cell-updates/s (FP64)", "value": value, "unit": "cell-updates/s",
+                "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"C5: {nx}x{nx}, M={M} ({N} moments), order {a.order}, BGK Kn 0.1, "
+                                       "walls theta=1; step = FS iteration + residual + restrict/prolong pair",
+                           "global_cells": nx * nx, "parallelism": f"column strips x{nstrips} "
+                           + ("(one per rank, peer memory over NVLink)" if world > 1 else "(one process)"),
+                           "strip_bounds": level.bounds,
+                           "l2": "inputs larger than L2 (field %.2f GB)" % (nx * nx * (N + 4) * 8 / 1e9),
+                           "sweep": "band dataflow across strips, exact lexicographic GS order"},
+                "breakdown_ms": {"fast_sweep+residual (strips, fenced)": sweep_med, "restrict_prolong": xfer_med},
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         reference_arm(a)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or a.strips:
+        strips_arm(a)
     else:
         ours(a)
 

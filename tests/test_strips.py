@@ -1,7 +1,11 @@
-"""Row-strip multi-rank path (world_size 2, gloo, CPU): the pipelined
-exact-order sweep over strips reproduces the serial fast_sweep_step bit for
-bit (per-cell updates by the CPU oracle), for first and second order and a
-non-empty rhs; the halo exchange reproduces the serial residual."""
+"""Multi-rank host layer of the strip partition (paper_2206_13164_b200/strips.py)
+on CPU: world_size 2 over gloo, the collectives the GPU path uses (IPC
+handle all-gather, barriers, the scalar reductions of total_mass and
+residual_norm combined from per-strip values).  The per-strip values are the
+oracle's own total_mass / residual_norm on each strip's sub-grid, so the
+combination is checked against the oracle on the whole level.  The device
+side of the partition (one kernel over all strips, bitwise equal to the
+single-field sweep) is tests/test_gpu_strips.py."""
 import os
 import socket
 
@@ -9,7 +13,9 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from helpers import BGK, SHAKHOV, Grid, Oracle, cavity_ctx, smooth_field
+from helpers import BGK, Grid, Oracle, c5_field, cavity_ctx
+
+from paper_2206_13164_b200.strips import StripComm, combine_mass, combine_norm, strip_bounds
 
 
 def _free_port():
@@ -20,65 +26,72 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, case, out_q):
-    import torch.distributed as dist
+def sub_grid(g: Grid, i0: int, i1: int) -> Grid:
+    dx = g.dx[i0:i1].copy()
+    return Grid(i1 - i0, g.ny, float(np.sum(dx)), g.Ly, dx, g.dy.copy(), g.xc[i0:i1].copy(), g.yc.copy())
 
-    from paper_2206_13164_b200.strips import Exchange, StripPartition, gather_strips, strip_fast_sweep
+
+def columns(a, g, i0, i1):
+    return a.reshape(g.ny, g.nx, -1)[:, i0:i1].reshape(-1, a.shape[1])
+
+
+def _worker(rank, world, port, out_q):
+    import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        M, order, model, nx, ny, use_rhs, chunk = case
+        comm = StripComm(dist)
+        # IPC handle exchange: every rank sees every rank's 320-byte handle
+        mine = bytes([rank + 1]) * 320
+        handles = comm.allgather_bytes(mine)
+        ok_handles = [h == bytes([r + 1]) * 320 for r, h in enumerate(handles)]
+        calls = []
+        comm.fence(lambda: calls.append(1))
+        # per-strip scalars on this rank's strip, combined across ranks
+        M, nx, ny = 5, 96, 10
+        g = Grid.uniform(nx, ny, 1.0, 0.7)
+        b = strip_bounds(nx, world)
+        i0, i1 = b[rank], b[rank + 1]
         O = Oracle("port")
-        g = Grid.uniform(nx, ny)
-        ctx = cavity_ctx(M, order, model, kn=0.3, prandtl=2.0 / 3.0 if model == SHAKHOV else 1.0,
-                         bottom_theta=1.2)
-        c, p = smooth_field(g, M, seed=nx + ny + M, amp=0.08)
-        rhs = (c * 1e-3, p.copy()) if use_rhs else None
-        part = StripPartition(nx, ny, world, order)
-        ex = Exchange(dist)
-        cc, pp = c.copy(), p.copy()
-
-        def update(cells):
-            O.sweep_cells(ctx, g, cc, pp, cells, rhs=rhs)
-
-        strip_fast_sweep(part, rank, ex, cc, pp, update, chunk=chunk)
-        full = gather_strips(part, rank, ex, cc, pp)
+        octx = cavity_ctx(M, 1, BGK, kn=0.1, lid=0.1)
+        c, p = c5_field(nx, ny, M, seed=4)
+        res = O.residual(octx, g, c, p)
+        sg = sub_grid(g, i0, i1)
+        mass = combine_mass(comm, [O.total_mass(sg, M, columns(c, g, i0, i1))])
+        norm = combine_norm(comm, [(O.residual_norm(M, sg, columns(res, g, i0, i1), columns(p, g, i0, i1)), sg.Lx)],
+                            g.Lx, g.Ly)
         if rank == 0:
-            want_c, want_p, _ = O.fast_sweep(ctx, g, c, p, rhs=rhs)
-            out_q.put((bool(np.array_equal(full[0], want_c)), bool(np.array_equal(full[1], want_p)),
-                       float(np.max(np.abs(full[0] - want_c)))))
+            out_q.put((ok_handles, calls, b, mass, O.total_mass(g, M, c), norm, O.residual_norm(M, g, res, p)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", [
-    (3, 1, BGK, 10, 8, False, 3),
-    (3, 2, BGK, 9, 12, False, 4),
-    (5, 2, SHAKHOV, 8, 8, True, 8),
-])
-def test_strip_sweep_matches_serial(case):
+def test_strip_layer_world2_gloo():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for pr in procs:
         pr.start()
     try:
-        eq_c, eq_p, diff = q.get(timeout=240)
+        ok_handles, calls, b, mass, want_mass, norm, want_norm = q.get(timeout=240)
     finally:
         for pr in procs:
             pr.join(timeout=60)
-    assert eq_c and eq_p, diff
+    assert all(ok_handles) and calls == [1]
+    assert b == [0, 64, 96]
+    assert mass == pytest.approx(want_mass, rel=1e-14)
+    assert norm == pytest.approx(want_norm, rel=1e-13)
 
 
-def test_partition_geometry():
-    from paper_2206_13164_b200.strips import StripPartition
-    part = StripPartition(16, 16, 4, 2)
-    assert part.rows == [(0, 4), (4, 8), (8, 12), (12, 16)]
-    assert part.halo == 2
-    assert part.halo_rows(0, from_high=False) == []
-    assert part.halo_rows(1, from_high=False) == [2, 3]
-    assert part.boundary_rows(1, toward_high=True) == [6, 7]
+def test_strip_bounds():
+    assert strip_bounds(2048, 1) == [0, 2048]
+    assert strip_bounds(2048, 8) == [256 * k for k in range(9)]
+    assert strip_bounds(160, 2) == [0, 96, 160]
+    b = strip_bounds(2048, 3)
+    assert b[-1] == 2048 and all((y - x) % 32 == 0 and y > x for x, y in zip(b, b[1:]))
     with pytest.raises(ValueError):
-        StripPartition(16, 14, 4, 1)
+        strip_bounds(100, 2)
+    with pytest.raises(ValueError):
+        strip_bounds(64, 3)  # more ranks than bands
