@@ -27,8 +27,8 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-# the FS iteration and the residual of a step as one launch (MOMG_FUSED=0: two)
-FUSED = os.environ.get("MOMG_FUSED", "1") != "0"
+# the FS iteration and the residual of a step as one launch (momg_fast_sweep_residual)
+FUSED = True
 sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402

@@ -210,16 +210,15 @@ int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const i
                                     long long* evals, momg_err* err);
 
 /* ---- execution strategy of fast_sweep (same results either way) -------- */
-/* 1 (default): one persistent dataflow kernel per call (band tasks at first
-   order, M <= 5; wavefront items otherwise); 3: persistent wavefront items
-   only; 2: persistent warp-per-cell kernels only; 0: one launch per
-   anti-diagonal (simple reference strategy).  Env MOMG_SWEEP=diag selects 0,
-   MOMG_BAND=0 disables the band tasks. */
+/* 1 (default): one persistent dataflow kernel per call (the band kernels for
+   M <= 5, thread-per-face M = 6, warp-per-cell M = 7, 8); 2: the same without
+   the band kernels (thread-per-face / warp-per-cell for every M); 0: one launch
+   per anti-diagonal (the simple reference strategy; env MOMG_SWEEP=diag). */
 int momg_set_sweep_mode(int mode);
 
 /* ---- instrumentation --------------------------------------------------- */
-/* debug: %globaltimer stamps of the first cap work items of the split
-   persistent sweep ([item][4]: start, dependencies ready, faces, update) */
+/* debug: %globaltimer stamps of the first cap band tasks of the band sweep
+   ([task][32]: loop start / end, steps, per-phase sums; tools/trace_band.py) */
 int momg_debug_trace(long long cap);
 long long momg_debug_trace_read(unsigned long long* host, long long n);
 /* number of kernels this library has launched since load (gpu_launches) */

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
   const int tid = threadIdx.x;
   const int warp = tid >> 5, g = warp / P, q = warp % P, c = tid & 31;
   const int ntasks = plan.nsweeps * plan.nbands;
-  const CellAddr fa{nullptr, f.c, f.p, plan.ver}, ra{nullptr, rhsf.c, rhsf.p, plan.ver};
+  const CellAddr<> fa{nullptr, f.c, f.p, plan.ver}, ra{nullptr, rhsf.c, rhsf.p, plan.ver};
   const bool has_rhs = plan.has_rhs != 0;
   const bool o2 = plan.order == 2;
   for (;;) {
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
     if (task >= ntasks || s_stop) return;
     const int s = task / plan.nbands, k = task % plan.nbands;
     const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
-    BandGeo b;
+    BandGeo<> b;
     b.nx = f.nx;
     b.ny = f.ny;
     b.k = k;

@@ -33,32 +33,37 @@
 namespace momg_gpu {
 namespace sp {
 
-// Global addresses of a cell handle (flat field, or strip table)
+// Global addresses of a cell handle (ST: strip table; else one flat field)
+template <bool ST = false>
 struct CellAddr {
+  static constexpr bool kStrips = ST;
   const StripTab* st;
   double* c;
   double* p;
   unsigned* ver;
+  template <class T>
+  static __device__ __forceinline__ T* tab(T* const* a, int h) {
+    return (T*)__ldg((const unsigned long long*)&a[h >> kStripShift]);
+  }
   __device__ __forceinline__ double* cptr(int h, int NP) const {
-    return st ? (double*)__ldg((const unsigned long long*)&st->c[h >> kStripShift]) + (size_t)(h & kStripMask) * NP
-              : c + (size_t)h * NP;
+    if constexpr (ST) return tab(st->c, h) + (size_t)(h & kStripMask) * NP;
+    else return c + (size_t)h * NP;
   }
   __device__ __forceinline__ double* pptr(int h) const {
-    return st ? (double*)__ldg((const unsigned long long*)&st->p[h >> kStripShift]) + (size_t)(h & kStripMask) * 4
-              : p + (size_t)h * 4;
+    if constexpr (ST) return tab(st->p, h) + (size_t)(h & kStripMask) * 4;
+    else return p + (size_t)h * 4;
   }
   __device__ __forceinline__ unsigned* vptr(int h) const {
-    return st ? (unsigned*)__ldg((const unsigned long long*)&st->ver[h >> kStripShift]) + (h & kStripMask)
-              : ver + h;
+    if constexpr (ST) return tab(st->ver, h) + (h & kStripMask);
+    else return ver + h;
   }
   __device__ __forceinline__ double* ocptr(int h, int NP, double* flat) const {
-    return st ? (double*)__ldg((const unsigned long long*)&st->oc[h >> kStripShift]) +
-                    (size_t)(h & kStripMask) * NP
-              : flat + (size_t)h * NP;
+    if constexpr (ST) return tab(st->oc, h) + (size_t)(h & kStripMask) * NP;
+    else return flat + (size_t)h * NP;
   }
   __device__ __forceinline__ double* opptr(int h, double* flat) const {
-    return st ? (double*)__ldg((const unsigned long long*)&st->op[h >> kStripShift]) + (size_t)(h & kStripMask) * 4
-              : flat + (size_t)h * 4;
+    if constexpr (ST) return tab(st->op, h) + (size_t)(h & kStripMask) * 4;
+    else return flat + (size_t)h * 4;
   }
 };
 
@@ -101,20 +106,41 @@ struct BandLayout {
   static constexpr size_t bytes = (size_t)(PRE + 2 * PRE_N * 32) * sizeof(double);
 };
 
+template <bool ST = false>
 struct BandGeo {
   int nx, ny, k, bw;
   bool i_up, j_up;
   const StripTab* st = nullptr;
+  // strip of the halo column (slot -1), of the band's own columns and of the
+  // next band's first column (slot bw): strips are whole bands, so a task
+  // touches at most these three (set per task by strips_init)
+  int r0 = 0, r1 = 0, r2 = 0, i00 = 0, i01 = 0, i02 = 0, w0 = 0, w1 = 0, w2 = 0;
+  __device__ __forceinline__ void strip_of(int slot, int* r, int* i0, int* w) const {
+    const int ir = min(max(bw * k + slot, 0), nx - 1);
+    const int i = i_up ? ir : nx - 1 - ir;
+    const int n = __ldg(&st->n);
+    int q = 0;
+#pragma unroll 1
+    for (int t = 1; t < n; ++t) q += i >= __ldg(&st->i0[t]) ? 1 : 0;
+    *r = q;
+    *i0 = __ldg(&st->i0[q]);
+    *w = __ldg(&st->i0[q + 1]) - *i0;
+  }
+  __device__ __forceinline__ void strips_init() {
+    if constexpr (!ST) return;
+    strip_of(-1, &r0, &i00, &w0);
+    strip_of(0, &r1, &i01, &w1);
+    strip_of(bw, &r2, &i02, &w2);
+  }
   // rotated cell (ir = 32k + slot, jr = dd - ir) -> cell handle, or -1
   __device__ __forceinline__ int cell(int slot, int dd) const {
     const int ir = bw * k + slot, jr = dd - ir;
     if (ir < 0 || ir >= nx || jr < 0 || jr >= ny) return -1;
     const int i = i_up ? ir : nx - 1 - ir, j = j_up ? jr : ny - 1 - jr;
-    if (!st) return j * nx + i;
-    const int n = __ldg(&st->n);
-    int r = 0;
-    for (int t = 1; t < n; ++t) r += i >= __ldg(&st->i0[t]) ? 1 : 0;
-    const int i0 = __ldg(&st->i0[r]), w = __ldg(&st->i0[r + 1]) - i0;
+    if constexpr (!ST) return j * nx + i;
+    const int r = slot < 0 ? r0 : (slot >= bw ? r2 : r1);
+    const int i0 = slot < 0 ? i00 : (slot >= bw ? i02 : i01);
+    const int w = slot < 0 ? w0 : (slot >= bw ? w2 : w1);
     return (r << kStripShift) | (j * w + i - i0);
   }
 };
@@ -142,8 +168,8 @@ __device__ __forceinline__ bool band_stop(const DevErr* err) {
 // parameters into prm[(slot - s0) * 4 ..], once the cell's counter reaches
 // `need` (0: no wait).  All of a warp's polls, then all of its loads, are in
 // flight together.
-template <int M, int MAXS>
-__device__ __forceinline__ void band_load(const CellAddr& fld, const BandGeo& b, int dd, int s0, int ns,
+template <int M, int MAXS, class Addr, class Geo>
+__device__ __forceinline__ void band_load(const Addr& fld, const Geo& b, int dd, int s0, int ns,
                                           unsigned need, double* vec, int vstride, double* prm, int wi, int nw,
                                           DevErr* err, int poll_ns, unsigned jit = 0, bool sys = false) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, H = (N + 31) / 32;
@@ -161,7 +187,7 @@ __device__ __forceinline__ void band_load(const CellAddr& fld, const BandGeo& b,
     // measured slower: the spinning warps slow the SM's memory pipeline)
     const unsigned* a = fld.vptr(my_cell);
     long long polls = 0;
-    while (ld_relaxed_s(a, sys) < need) {
+    while (ld_relaxed_s(a, Addr::kStrips && sys) < need) {
       if (band_stop(err)) break;
       if (++polls > (1LL << 26)) {
         tc::raise(err, E_ERROR, W_DEADLOCK, my_cell % b.nx, my_cell / b.nx, (double)need);
@@ -169,7 +195,7 @@ __device__ __forceinline__ void band_load(const CellAddr& fld, const BandGeo& b,
       }
       if (poll_ns) __nanosleep(poll_ns);
     }
-    (void)ld_acquire_s(a, sys);
+    (void)ld_acquire_s(a, Addr::kStrips && sys);
   }
   __syncwarp();
   double r[MAXS][H];
@@ -211,8 +237,8 @@ __device__ __forceinline__ void band_load(const CellAddr& fld, const BandGeo& b,
 // and bases are in OLD1 / PO, into a PRE block: one step ahead of the cell
 // update, by a warp that is otherwise idle, so that pow / sqrt / divisions
 // are off the critical path.
-template <int M, int BW>
-__device__ __forceinline__ void band_pre(const DevField& f, const DevCtx& ctx, const BandGeo& b, int dd,
+template <int M, int BW, class Geo>
+__device__ __forceinline__ void band_pre(const DevField& f, const DevCtx& ctx, const Geo& b, int dd,
                                          const double* OLD1, const double* PO, double* pre) {
   const int c = threadIdx.x & 31;
   const int ir = BW * b.k + c, jr = dd - ir;
@@ -244,8 +270,8 @@ __device__ __forceinline__ void band_pre(const DevField& f, const DevCtx& ctx, c
 // update succeeded (ok).  Warp w of 16 stores cells 2w and 2w+1, lane =
 // coefficient (coalesced).  Runs at the start of the next step on all warps,
 // so the update's critical path ends with its last projection pass.
-template <int M>
-__device__ __forceinline__ void band_writeback(const CellAddr& f, const BandGeo& b, int dd, const double* V,
+template <int M, class Addr, class Geo>
+__device__ __forceinline__ void band_writeback(const Addr& f, const Geo& b, int dd, const double* V,
                                                const double* PV, const int* ok, int warp) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3;
   const int lane = threadIdx.x & 31;
@@ -275,7 +301,7 @@ __device__ __forceinline__ void band_writeback(const CellAddr& f, const BandGeo&
 // counter, tasks are (band, chunk of diagonals) so all SMs have work, and the
 // previous diagonal's states (V) are the old ones, copied there by group 0
 // after it assembles R = Q - sum of the face fluxes, which it stores to `out`.
-template <int M, int BW, bool RES = false>
+template <int M, int BW, bool RES = false, bool ST = false>
 __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, DevErr* err, BandPlan plan,
                                                       DevField out) {
   static_assert(BW == 16 || BW == 32, "band width: 16 or 32 columns");
@@ -299,8 +325,8 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
   const int ntasks = sweep_tasks + plan.nchunks * plan.nk;
   const unsigned ep = plan.epoch;  // counters count from here (0: zeroed per launch)
   const unsigned rneed = RES ? 0u : ep + (unsigned)plan.nsweeps;
-  const bool sys = plan.sys != 0;
-  const CellAddr fa{plan.strips, f.c, f.p, plan.ver};
+  const bool sys = ST && plan.sys != 0;
+  const CellAddr<ST> fa{plan.strips, f.c, f.p, plan.ver};
   for (;;) {
     if (tid == 0) {
       sched_jitter(plan.jitter, 1u);
@@ -316,7 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     // residual tasks walk the frame of the last sweep, whose wavefront they follow
     const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
     const int k = (dir == 0 || dir == 3 ? plan.kb_up : plan.kb_dn) + (res ? rtask : task) % plan.nk;
-    BandGeo b;
+    BandGeo<ST> b;
     b.nx = f.nx;
     b.ny = f.ny;
     b.k = k;
@@ -324,6 +350,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     b.i_up = dir == 0 || dir == 3;  // kSweepDirs (single_level.cpp:116-117)
     b.j_up = dir == 0 || dir == 1;
     b.st = plan.strips;
+    b.strips_init();
     const int ir = BW * k + c;
     int dfirst = BW * k, dlast = min(BW * k + BW - 1, f.nx - 1) + f.ny - 1;
     if (res) {
@@ -350,7 +377,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         if (cl >= 0 && need) {
           long long polls = 0;
           const unsigned* a = fa.vptr(cl);
-          while (ld_relaxed_s(a, sys) < need) {
+          while (ld_relaxed_s(a, ST && sys) < need) {
             if (band_stop(err)) break;
             if (++polls > (1LL << 26)) {
               tc::raise(err, E_ERROR, W_DEADLOCK, cl % f.nx, cl / f.nx, (double)need);
@@ -358,7 +385,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
             }
             __nanosleep(kPrologueSleepNs);
           }
-          (void)ld_acquire_s(a, sys);
+          (void)ld_acquire_s(a, ST && sys);
         }
       }
     }
@@ -545,7 +572,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
         if (g == 1 && q == 0 && d > dfirst && c < BW) {
           sched_jitter(plan.jitter, (unsigned)d);
           const int cl = b.cell(c, d - 1);
-          if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, sys);
+          if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, ST && sys);
         }
         {
           const double* pre = smem + LY::PRE + (d & 1) * PRE_N * 32 + c;
@@ -621,7 +648,7 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     __syncthreads();
     if (!res && warp == 4 && c < BW) {  // publish the last step
       const int cl = b.cell(c, dlast);
-      if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, sys);
+      if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, ST && sys);
     }
     if (tr) {
       unsigned long long* o = plan.trace + (size_t)task * 32;

@@ -414,16 +414,12 @@ int tc_sweep_blocks(const void* kernel, size_t smem, int threads = tc::VS);
 tc::SegPlan tc_seg_plan(momg_field* f, int seg = tc::SEG);
 template <int M>
 constexpr bool use_split() { return M <= 5; }
-bool split_sweep_enabled();
 unsigned long long* trace_buffer(long long* cap);
-void poll_tuning(int* split_wait, int* poll_ns);
 unsigned sched_jitter_seed();
 void band_scratch(momg_field* f, unsigned** ver, unsigned** next);
+// the band kernels for M <= 5 (momg_set_sweep_mode 1, the default); mode 2
+// runs the thread-per-face / warp-per-cell kernels, mode 0 per-diagonal launches
 bool band_sweep_enabled();
-bool band2_enabled();
-bool band_residual_enabled();
-void set_band_mode(int m);
-const uint32_t* split_schedule(momg_field* f, int nsweeps, const int* dirs, int radius, int seg);
 
 // ---------------------------------------------------- templated launchers
 template <int M>
@@ -474,8 +470,7 @@ struct Launch {
   // the fused path does not apply (the caller runs the two operations).
   static bool sweep_res(const DevCtx& ctx, momg_field* f, const int* order, momg_field* out, int iters) {
     if constexpr (use_split<M>()) {
-      if (ctx.order == 1 && iters >= 1 && iters <= 4 && persistent_sweep_enabled() && split_sweep_enabled() &&
-          band_sweep_enabled() && band_residual_enabled()) {
+      if (ctx.order == 1 && iters >= 1 && iters <= 4 && band_sweep_enabled()) {
         static bool battr = false;
         if (!battr) {
           set_smem(sp::k5_band<M, 32>, sp::BandLayout<M>::bytes);
@@ -491,8 +486,6 @@ struct Launch {
           bp.dirs[s] = order[s & 3];
           bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
         }
-        int sw = 0;
-        poll_tuning(&sw, &bp.poll_ns);
             bp.jitter = sched_jitter_seed();
         const int ndiag = std::min(31, f->nx - 1) + f->ny;
         bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
@@ -517,7 +510,7 @@ struct Launch {
   }
   static void residual(const DevCtx& ctx, const momg_field* f, momg_field* out) {
     if constexpr (use_split<M>()) {
-      if (ctx.order == 1 && band_sweep_enabled() && band_residual_enabled()) {
+      if (ctx.order == 1 && band_sweep_enabled()) {
         // the band kernel in residual mode: (band, diagonal chunk) tasks
         static bool rattr = false;
         if (!rattr) {
@@ -569,7 +562,7 @@ struct Launch {
   // persistent kernel runs them as one launch so the sweeps overlap)
   static void sweep_n(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int* order, int iters) {
     if constexpr (use_split<M>()) {
-      if (!(persistent_sweep_enabled() && split_sweep_enabled()) || iters > 4) {
+      if (!band_sweep_enabled() || iters > 4) {
         for (int it = 0; it < iters; ++it) sweep1(ctx, f, rhs, order, 1);
         return;
       }
@@ -588,14 +581,8 @@ struct Launch {
       DevErr* err = momg_rt::err_dev();
       DevCtx c = ctx;
       if constexpr (use_split<M>()) {
-        if (persistent_sweep_enabled() && split_sweep_enabled()) {
-          static bool sattr = false;
-          if (!sattr) {
-            set_smem(sp::k4_sweep<M, 1>, sp::Layout<M>::bytes);
-            set_smem(sp::k4_sweep<M, 2>, sp::Layout<M>::bytes);
-            sattr = true;
-          }
-          if (ctx.order == 1 && !rhs && band_sweep_enabled()) {
+        if (band_sweep_enabled()) {
+          if (ctx.order == 1 && !rhs) {
             static bool battr = false;
             if (!battr) {
               set_smem(sp::k5_band<M, 32>, sp::BandLayout<M>::bytes);
@@ -612,8 +599,6 @@ struct Launch {
               bp.dirs[s] = order[s & 3];
               bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
             }
-            int sw = 0;
-            poll_tuning(&sw, &bp.poll_ns);
             bp.jitter = sched_jitter_seed();
             bp.trace = trace_buffer(&bp.trace_cap);
             bp.nchunks = 0;  // no fused residual tasks
@@ -624,7 +609,7 @@ struct Launch {
             momg_rt::count_launch(1);
             return;
           }
-          if (band_sweep_enabled() && band2_enabled()) {
+          {
             // second order and/or an FAS rhs: the 16-column band sweep
             sp::Band2Plan bp{};
             band_scratch(f, &bp.ver, &bp.next);
@@ -634,8 +619,6 @@ struct Launch {
             for (int s = 0; s < 16; ++s) bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
             bp.order = ctx.order;
             bp.has_rhs = rhs != nullptr;
-            int sw = 0;
-            poll_tuning(&sw, &bp.poll_ns);
             bp.jitter = sched_jitter_seed();
             if constexpr (M == 3) band2_launch_m3(fd, rd, c, err, bp, momg_rt::stream());
             else if constexpr (M == 4) band2_launch_m4(fd, rd, c, err, bp, momg_rt::stream());
@@ -643,29 +626,6 @@ struct Launch {
             momg_rt::count_launch(1);
             return;
           }
-          const tc::SegPlan p16 = tc_seg_plan(f, 32);
-          sp::SegPlan32 plan;
-          plan.diag_lo = p16.diag_lo;
-          plan.seg_start = p16.seg_start;
-          plan.ver = p16.ver;
-          plan.nd = p16.nd;
-          plan.nsweeps = 4 * iters;
-          plan.dirbits = 0;
-          for (int s = 0; s < 16; ++s) {
-            plan.dirs[s] = order[s & 3];
-            plan.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
-          }
-          plan.items = split_schedule(f, plan.nsweeps, plan.dirs, ctx.order == 2 ? 2 : 1, 32);
-          plan.trace = trace_buffer(&plan.trace_cap);
-          poll_tuning(&plan.split_wait, &plan.poll_ns);
-          const void* kern = ctx.order == 2 ? (const void*)sp::k4_sweep<M, 2> : (const void*)sp::k4_sweep<M, 1>;
-          int nb = tc_sweep_blocks(kern, sp::Layout<M>::bytes, sp::THREADS);
-          DevField fa = fd, ra = rd;
-          void* args[] = {&fa, &ra, &has_rhs, &c, &err, &plan};
-          momg_rt::note_launch(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(sp::THREADS), args, sp::Layout<M>::bytes,
-                                      momg_rt::stream()));
-          momg_rt::count_launch(1);
-          return;
         }
       }
       if (persistent_sweep_enabled()) {
@@ -812,7 +772,7 @@ struct Launch {
       if (ctx.order != 1) return false;
       static bool battr = false;
       if (!battr) {
-        set_smem(sp::k5_band<M, 32>, sp::BandLayout<M>::bytes);
+        set_smem(sp::k5_band<M, 32, false, true>, sp::BandLayout<M>::bytes);
         battr = true;
       }
       sp::BandPlan bp{};
@@ -824,8 +784,6 @@ struct Launch {
         bp.dirs[s] = L.order[s & 3];
         bp.dirbits |= (unsigned)(L.order[s & 3] & 3) << (2 * s);
       }
-      int sw = 0;
-      poll_tuning(&sw, &bp.poll_ns);
       bp.jitter = sched_jitter_seed();
       const int ndiag = std::min(31, L.geo.nx - 1) + L.geo.ny;
       bp.nchunks = std::max(1, (2 * 148 + L.nk - 1) / L.nk);
@@ -837,13 +795,13 @@ struct Launch {
       bp.kb_dn = L.kb_dn;
       bp.nk = L.nk;
       bp.sys = L.sys;
-      int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
+      int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32, false, true>, sp::BandLayout<M>::bytes, sp::THREADS);
       const int tasks = (bp.nsweeps + bp.nchunks) * bp.nk;
       if (nb > tasks) nb = tasks;
       DevCtx c = ctx;
       DevField none = L.geo;
       none.c = none.p = nullptr;
-      sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(
+      sp::k5_band<M, 32, false, true><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(
           L.geo, c, momg_rt::err_dev(), bp, none);
       momg_rt::note_launch(cudaGetLastError());
       momg_rt::count_launch(1);

@@ -380,7 +380,6 @@ bool persistent_sweep_enabled() {
   return g_sweep_mode == 1;
 }
 void set_sweep_mode(int m) { g_sweep_mode = m; }
-void set_split_mode(int m);
 void set_band_mode(int m);
 void set_trace(long long cap);
 long long read_trace(unsigned long long* host, long long n);
@@ -419,90 +418,7 @@ tc::SegPlan tc_seg_plan(momg_field* f, int seg) {
 
 }  // namespace momg_gpu
 
-// Dependency-level schedule of the split persistent sweep: work item = (sweep
-// s, anti-diagonal d, 32-cell segment).  level(item) = 1 + max level of the
-// items owning its cells' dependencies (the rule of sweep_persistent.cuh);
-// items sorted by (level, sweep-major index) form a topological order in
-// which sweep s+1 starts as soon as sweep s has passed its first cells.
-struct Schedule {
-  int nsweeps = 0, radius = 0, seg = 0;
-  int dirs[16] = {0};
-  uint32_t* dev = nullptr;
-};
-
 namespace momg_gpu {
-
-const uint32_t* split_schedule(momg_field* f, int nsweeps, const int* dirs, int radius, int seg) {
-  Schedule*& sc = f->schedule;
-  if (sc && sc->nsweeps == nsweeps && sc->radius == radius && sc->seg == seg &&
-      std::equal(dirs, dirs + nsweeps, sc->dirs))
-    return sc->dev;
-  if (!sc) sc = new Schedule();
-  if (sc->dev) cudaFree(sc->dev);
-  sc->nsweeps = nsweeps;
-  sc->radius = radius;
-  sc->seg = seg;
-  std::copy(dirs, dirs + nsweeps, sc->dirs);
-  const int nx = f->nx, ny = f->ny, nd = nx + ny - 1;
-  std::vector<int> dlo(nd), sstart(nd + 1);
-  int acc = 0;
-  for (int d = 0; d < nd; ++d) {
-    const int lo = d - (ny - 1) > 0 ? d - (ny - 1) : 0;
-    const int hi = d < nx - 1 ? d : nx - 1;
-    dlo[d] = lo;
-    sstart[d] = acc;
-    acc += (hi - lo + 1 + seg - 1) / seg;
-  }
-  sstart[nd] = acc;
-  const int per = acc;
-  auto item_of = [&](int s, int i, int j) {
-    const int dir = dirs[s];
-    const bool iu = dir == 0 || dir == 3, ju = dir == 0 || dir == 1;
-    const int ii = iu ? i : nx - 1 - i, jj = ju ? j : ny - 1 - j;
-    const int d = ii + jj;
-    return s * per + sstart[d] + (ii - dlo[d]) / seg;
-  };
-  std::vector<int> level((size_t)per * nsweeps, 0);
-  for (int s = 0; s < nsweeps; ++s) {
-    const int dir = dirs[s];
-    const bool iu = dir == 0 || dir == 3, ju = dir == 0 || dir == 1;
-    for (int d = 0; d < nd; ++d) {
-      const int hi = d < nx - 1 ? d : nx - 1;
-      for (int sg = 0; sstart[d] + sg < sstart[d + 1]; ++sg) {
-        const int id = s * per + sstart[d] + sg;
-        int lv = 0;
-        for (int ii = dlo[d] + sg * seg; ii <= hi && ii < dlo[d] + (sg + 1) * seg; ++ii) {
-          const int jj = d - ii;
-          const int i = iu ? ii : nx - 1 - ii, j = ju ? jj : ny - 1 - jj;
-          if (s > 0) lv = std::max(lv, level[item_of(s - 1, i, j)] + 1);
-          for (int dist = 1; dist <= radius; ++dist) {
-            const int nb[4][2] = {{i - dist, j}, {i + dist, j}, {i, j - dist}, {i, j + dist}};
-            for (int q = 0; q < 4; ++q) {
-              const int ni = nb[q][0], nj = nb[q][1];
-              if (ni < 0 || ni >= nx || nj < 0 || nj >= ny) continue;
-              const bool before = q < 2 ? (iu ? ni < i : ni > i) : (ju ? nj < j : nj > j);
-              if (before) lv = std::max(lv, level[item_of(s, ni, nj)] + 1);
-              else if (s > 0) lv = std::max(lv, level[item_of(s - 1, ni, nj)] + 1);
-            }
-          }
-        }
-        level[id] = lv;
-      }
-    }
-  }
-  std::vector<int> ids((size_t)per * nsweeps);
-  for (size_t k = 0; k < ids.size(); ++k) ids[k] = (int)k;
-  std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) { return level[a] < level[b]; });
-  std::vector<uint32_t> packed(ids.size());
-  for (size_t k = 0; k < ids.size(); ++k) {
-    const int s = ids[k] / per, r = ids[k] % per;
-    const int d = (int)(std::upper_bound(sstart.begin(), sstart.end(), r) - sstart.begin()) - 1;
-    packed[k] = ((uint32_t)s << 28) | ((uint32_t)(r - sstart[d]) << 16) | (uint32_t)d;
-  }
-  cudaMalloc(&sc->dev, packed.size() * sizeof(uint32_t));
-  cudaMemcpy(sc->dev, packed.data(), packed.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
-  return sc->dev;
-}
 
 static unsigned long long* g_trace = nullptr;
 static long long g_trace_cap = 0;
@@ -526,17 +442,6 @@ long long read_trace(unsigned long long* host, long long n) {
   return n;
 }
 
-// persistent-sweep polling policy (MOMG_POLL="split,ns"; tuning/debug)
-void poll_tuning(int* split_wait, int* poll_ns) {
-  static int sw = -1, ns = 0;
-  if (sw < 0) {
-    sw = 0;
-    if (const char* e = std::getenv("MOMG_POLL")) std::sscanf(e, "%d,%d", &sw, &ns);
-  }
-  *split_wait = sw;
-  *poll_ns = ns;
-}
-
 // schedule perturbation for the race stress tests (MOMG_JITTER=<seed>, read
 // at every launch): the band kernels sleep pseudo-random 0-2 us before task
 // claims, publications and polls, so the inter-CTA protocol runs under other
@@ -555,47 +460,10 @@ void band_scratch(momg_field* f, unsigned** ver, unsigned** next) {
   *next = f->band_next;
 }
 
-static int g_band = -1;
-bool band_sweep_enabled() {
-  if (g_band < 0) {
-    const char* e = std::getenv("MOMG_BAND");
-    g_band = (e && std::string(e) == "0") ? 0 : 1;
-  }
-  return g_band == 1;
-}
+// band kernels for M <= 5 (momg_set_sweep_mode: 1 on, 0 / 2 off)
+static int g_band = 1;
+bool band_sweep_enabled() { return g_band == 1 && persistent_sweep_enabled(); }
 void set_band_mode(int m) { g_band = m; }
-
-// first-order residual on the band kernel (MOMG_BAND_RES=0: k3_residual)
-bool band_residual_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("MOMG_BAND_RES");
-    on = (e && std::string(e) == "0") ? 0 : 1;
-  }
-  return on == 1;
-}
-
-// second-order / rhs sweeps on the 16-column band kernel (MOMG_BAND2=0: the
-// wavefront-item kernel k4_sweep)
-bool band2_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = std::getenv("MOMG_BAND2");
-    on = (e && std::string(e) == "0") ? 0 : 1;
-  }
-  return on == 1;
-}
-
-
-static int g_split = -1;
-bool split_sweep_enabled() {
-  if (g_split < 0) {
-    const char* e = std::getenv("MOMG_SPLIT");
-    g_split = (e && std::string(e) == "0") ? 0 : 1;
-  }
-  return g_split == 1;
-}
-void set_split_mode(int m) { g_split = m; }
 
 int tc_sweep_blocks(const void* kernel, size_t smem, int threads) {
   int per_sm = 0, dev = 0, sms = 0;
@@ -771,10 +639,6 @@ void field_free(momg_field* f) {
   cudaFree(f->sweep_order);
   cudaFree(f->seg_plan);
   cudaFree(f->seg_plan32);
-  if (f->schedule) {
-    cudaFree(f->schedule->dev);
-    delete f->schedule;
-  }
   cudaFree(f->sweep_ver);
   cudaFree(f->band_next);
   delete f;
@@ -843,9 +707,8 @@ long long momg_debug_trace_read(unsigned long long* host, long long n) {
   return momg_gpu::read_trace(host, n);
 }
 int momg_set_sweep_mode(int mode) {
-  if (mode < 0 || mode > 3) return MOMG_ERR_ARG;
+  if (mode < 0 || mode > 2) return MOMG_ERR_ARG;
   momg_gpu::set_sweep_mode(mode == 0 ? 0 : 1);
-  momg_gpu::set_split_mode(mode == 2 ? 0 : 1);
   momg_gpu::set_band_mode(mode == 1 ? 1 : 0);
   return MOMG_OK;
 }

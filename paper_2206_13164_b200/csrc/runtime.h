@@ -22,7 +22,6 @@ struct momg_field {
   unsigned* band_next = nullptr;    // band sweep: task counter (lazy)
   int* seg_plan = nullptr;          // thread-granular sweep: diag_lo | seg_start (lazy)
   int* seg_plan32 = nullptr;        // split sweep (32-cell segments)
-  struct Schedule* schedule = nullptr;  // split sweep: cached dependency-level item order
   cudaEvent_t ev_free = nullptr;        // overlapped transfers: last download of this field done
   // overlapped upload pending on the H2D copy stream: the library stream
   // waits on ev_ready the first time an entry point uses the field

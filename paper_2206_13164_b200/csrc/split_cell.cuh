@@ -515,163 +515,6 @@ __device__ __forceinline__ int face_core(const DevCtx& ctx, int g, int q, int ax
   return fail;
 }
 
-template <int M, int ORDER, int AXIS, bool RHS>
-__device__ __forceinline__ int face_split(const DevField& f, const DevCtx& ctx, int g, int q, bool valid,
-                                          int i, int j, double* L, double* U, double* F, double* SB,
-                                          const DevField* rhsf, double* RB, P4* cp_out,
-                                          unsigned long long* stamp = nullptr) {
-  constexpr int NP = (Gen<M>::N + 3) & ~3;
-  const bool high = g & 1;
-  const int n = AXIS == 0 ? f.nx : f.ny;
-  const int pos = AXIS == 0 ? i : j;
-  const size_t cell = (size_t)j * f.nx + i;
-  const size_t stride = AXIS == 0 ? 1 : (size_t)f.nx;
-  int klo, khi;
-  krange<M>(q, &klo, &khi);
-  int branch = B_NONE;
-  int fail = W_NONE;
-  P4 cp{}, lp{}, rp{}, fp{};
-  const double* xc = AXIS == 0 ? f.xc : f.yc;
-  const double* dd = AXIS == 0 ? f.dx : f.dy;
-  // ---- phase 0: face states (spatial.cpp:34-80) into L / U.
-  // Each lane (= cell) resolves its face geometry and publishes a small
-  // descriptor in warp-private scratch (this group's F vector, unused until
-  // phase 3).  The warp then loads the coefficient records of cells
-  // 8q..8q+7 cooperatively (lane = coefficient, coalesced 448-byte reads),
-  // all of a batch in flight at once, while each lane fetches its cell's
-  // parameter records and decides the second-order reconstruction
-  // (safe_face_state); a second descriptor pass applies the decisions and
-  // transposes into the interleaved vectors.  Group 0 (x-low face: the upper
-  // cell is the cell itself) also stages the cell state (and rhs) in SB / RB.
-  {
-    constexpr int N = Gen<M>::N;
-    constexpr int H = (N + 31) / 32;
-    constexpr int B = ORDER == 2 ? 2 : 4;  // cells per load batch
-    const int lane = threadIdx.x & 31;
-    double* Fbase = F - lane;
-    // 128 doubles per warp: fits the smallest F vector (M=3: 20 x 33)
-    static_assert(4 * 128 <= N * SPV, "phase-0 scratch exceeds the F vector");
-    double* DaL = Fbase + q * 128;
-    double* DaU = DaL + 32;
-    int* Dcl = reinterpret_cast<int*>(DaL + 64);
-    int* Dcu = Dcl + 32;
-    int* Dfl = Dcl + 64;
-    int* Ddec = Dcl + 96;
-    bool at_wall = false, rl = false, ru = false;
-    size_t cl = cell, cu = cell;
-    int pl = pos, pu = pos;
-    if (valid) {
-      at_wall = high ? pos == n - 1 : pos == 0;
-      pl = high ? pos : pos - 1;
-      pu = pl + 1;
-      cl = (high || at_wall) ? cell : cell - stride;  // wall: the cell itself
-      cu = at_wall ? cell : cl + stride;
-      rl = !at_wall && ORDER == 2 && pl > 0 && pl < n - 1;
-      ru = !at_wall && ORDER == 2 && pu > 0 && pu < n - 1;
-    }
-    Dcl[lane] = (int)cl;
-    Dcu[lane] = (int)cu;
-    Dfl[lane] = (valid ? 1 : 0) | (at_wall ? 2 : 0) | (rl ? 4 : 0) | (ru ? 8 : 0);
-    __syncwarp();
-    double* Lb = L - lane;
-    double* Ub = U - lane;
-    double* Sb = SB ? SB - lane : nullptr;
-    double* Rb = RB ? RB - lane : nullptr;
-#pragma unroll
-    for (int t0 = 0; t0 < 8; t0 += B) {
-      // (1) issue every coefficient load of the batch
-      double lk[B][H], uk[B][H], llk[B][H], uuk[B][H], rk[B][H];
-#pragma unroll
-      for (int t = 0; t < B; ++t) {
-        const int cc = 8 * q + t0 + t;
-        const int fl = Dfl[cc];
-        const bool ok = fl & 1, wall = fl & 2, el = fl & 4, eu = fl & 8;
-        const double* gl = f.c + (size_t)Dcl[cc] * NP;
-        const double* gu = f.c + (size_t)Dcu[cc] * NP;
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-          const int k = lane + 32 * h;
-          const bool in = ok && k < N;
-          lk[t][h] = in ? __ldcg(gl + k) : 0.0;
-          uk[t][h] = (in && !wall) ? __ldcg(gu + k) : 0.0;
-          llk[t][h] = (in && el) ? __ldcg(gl - stride * NP + k) : 0.0;
-          uuk[t][h] = (in && eu) ? __ldcg(gu + stride * NP + k) : 0.0;
-          rk[t][h] = (RHS && g == 0 && in) ? __ldcg(rhsf->c + (size_t)Dcu[cc] * NP + k)  /* g == 0: cu is the cell */ : 0.0;
-        }
-      }
-      // (2) first batch: this lane's parameter records and reconstruction decision
-      if (t0 == 0) {
-        int dec = 0;
-        double aL = 0.0, aU = 0.0;
-        if (valid) {
-          cp = tc::ldp<true>(f.p + cell * 4);
-          P4 pL = cp, pU = cp, pLL = cp, pUU = cp;
-          if (!at_wall) {
-            pL = tc::ldp<true>(f.p + cl * 4);
-            pU = tc::ldp<true>(f.p + cu * 4);
-          }
-          if (rl) pLL = tc::ldp<true>(f.p + (cl - stride) * 4);
-          if (ru) pUU = tc::ldp<true>(f.p + (cu + stride) * 4);
-          branch = at_wall ? B_WALL : B_HALF;
-          lp = pL;
-          rp = pU;
-          if (rl) {
-            const double hl = xc[pl + 1] - xc[pl - 1], offL = 0.5 * dd[pl];
-            P4 w;
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) w.v[qq] = pL.v[qq] + offL * ((pU.v[qq] - pLL.v[qq]) / hl);
-            if (w.v[3] > 0.0) {
-              dec |= 1;
-              lp = w;
-              aL = offL / hl;
-            }
-          }
-          if (ru) {
-            const double hu = xc[pu + 1] - xc[pu - 1], offU = -0.5 * dd[pu];
-            P4 w;
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) w.v[qq] = pU.v[qq] + offU * ((pUU.v[qq] - pL.v[qq]) / hu);
-            if (w.v[3] > 0.0) {
-              dec |= 2;
-              rp = w;
-              aU = offU / hu;
-            }
-          }
-        }
-        Ddec[lane] = dec;
-        DaL[lane] = aL;
-        DaU[lane] = aU;
-        __syncwarp();
-      }
-      // (3) apply the decisions and transpose
-#pragma unroll
-      for (int t = 0; t < B; ++t) {
-        const int cc = 8 * q + t0 + t;
-        const int fl = Dfl[cc];
-        if (!(fl & 1)) continue;
-        const bool wall = fl & 2;
-        const int dec = Ddec[cc];
-        const double aL = DaL[cc], aU = DaU[cc];
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-          const int k = lane + 32 * h;
-          if (k < N) {
-            const double l = lk[t][h], u = uk[t][h];
-            Lb[k * SPV + cc] = (dec & 1) ? fma(aL, u - llk[t][h], l) : l;
-            if (!wall) Ub[k * SPV + cc] = (dec & 2) ? fma(aU, uuk[t][h] - l, u) : u;
-            if (g == 0) Sb[k * SPV + cc] = wall ? l : u;
-            if (RHS && g == 0) Rb[k * SPV + cc] = rk[t][h];
-          }
-        }
-      }
-    }
-  }
-  gbar(g);
-  if (stamp) stamp[0] = gtimer0();
-  fail = face_core<M>(ctx, g, q, AXIS, high, branch, fail, lp, rp, cp, L, U, F, stamp);
-  *cp_out = cp;
-  return fail;
-}
 
 // ------------------------------------------------------------- cell update
 // sweep_cell (single_level.cpp:103-111): local dt, residual assembly
@@ -859,21 +702,6 @@ __device__ __forceinline__ int update_split(const DevField& f, const DevField* r
   return (valid && !good && fail == W_NONE) ? W_DT_HALVING : fail;
 }
 
-// ------------------------------------------------ persistent split sweep
-struct SegPlan32 {
-  const int* diag_lo;
-  const int* seg_start;
-  unsigned* ver;
-  const uint32_t* items;  // work items in dependency-level order: s<<28 | seg<<16 | d
-  int nd;
-  int nsweeps;            // <= 16
-  int dirs[16];
-  unsigned dirbits;       // dirs[s] = (dirbits >> 2s) & 3 (no runtime-indexed param array)
-  unsigned long long* trace;  // optional [item][4] %globaltimer stamps (debug)
-  long long trace_cap;
-  int split_wait;  // 1: each face group waits only for its own stencil
-  int poll_ns;     // back-off between failed polls (0: spin)
-};
 
 __device__ __forceinline__ unsigned long long gtimer() {
 #ifdef TRACE_CLOCK  // SM cycle counter scaled to ns at 1965 MHz (per-SM, not global)
@@ -883,113 +711,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 #endif
-}
-
-template <int M, int ORDER>
-__global__ void __launch_bounds__(THREADS, 1) k4_sweep(DevField f, DevField rhs, int has_rhs, DevCtx ctx,
-                                                      DevErr* err, SegPlan32 plan) {
-  extern __shared__ __align__(128) double smem[];
-  __shared__ int s_stop;
-  constexpr int VEC = Layout<M>::VEC;
-  const int warp = threadIdx.x >> 5, g = warp / P, q = warp % P, c = threadIdx.x & 31;
-  double* L = smem + (g * 3 + 0) * VEC + c;
-  double* U = smem + (g * 3 + 1) * VEC + c;
-  double* F = smem + (g * 3 + 2) * VEC + c;
-  const int per_sweep = plan.seg_start[plan.nd];
-  const long long total = (long long)per_sweep * plan.nsweeps;
-  constexpr int radius = ORDER == 2 ? 2 : 1;
-  for (long long item = blockIdx.x; item < total; item += gridDim.x) {
-    if (threadIdx.x == 0) s_stop = *((volatile const int*)&err->code) != 0;
-    __syncthreads();
-    if (s_stop) return;
-    const bool tr = plan.trace && item < plan.trace_cap && threadIdx.x == 0;
-    if (tr) plan.trace[item * 8 + 0] = gtimer();
-    const uint32_t pk = plan.items[item];
-    const int s = (int)(pk >> 28);
-    const int seg = (int)((pk >> 16) & 0xfff);
-    const int d = (int)(pk & 0xffff);
-    const int dhi = d < f.nx - 1 ? d : f.nx - 1;
-    const int ii = plan.diag_lo[d] + seg * 32 + c;
-    const bool valid = ii <= dhi;
-    const int jj = d - ii;
-    const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
-    const bool i_up = dir == 0 || dir == 3, j_up = dir == 0 || dir == 1;  // kSweepDirs
-    const int i = valid ? (i_up ? ii : f.nx - 1 - ii) : 0;
-    const int j = valid ? (j_up ? jj : f.ny - 1 - jj) : 0;
-    // dependency wait (rule in sweep_persistent.cuh), per face group: the
-    // group polls exactly the cells its face stencil reads -- partition 1
-    // the cell itself, partition 0 the others (order 1: the face neighbour;
-    // order 2 also the reconstruction neighbours, spatial.cpp:34-50) -- and
-    // only the group's own barrier follows.  At first order the high-face
-    // groups (1, 3) read previous-sweep values only, so they usually start at
-    // once and leave the SM to the low-face groups on the critical path.
-    // Polls spin on relaxed loads; success is confirmed with acquire loads.
-    if (valid && (q == 0 || (q == 1 && (plan.split_wait || g == 0)))) {
-      const int axis = g >> 1, side = g & 1;
-      constexpr int NOFF = ORDER == 2 ? 3 : 1;
-      long long polls = 0;
-      for (int pass = 0; pass < 2; ++pass) {  // 0: relaxed spin, 1: acquire confirm
-        bool ok = false;
-        while (!ok) {
-          ok = true;
-          if (q == 1) {
-            const unsigned* a = plan.ver + j * f.nx + i;
-            if ((pass ? ld_acquire(a) : ld_relaxed(a)) < (unsigned)s) ok = false;
-          } else {
-#pragma unroll
-            for (int t = 0; t < NOFF; ++t) {
-              const int o = side ? (t == 0 ? 1 : t == 1 ? 2 : -1) : (t == 0 ? -1 : t == 1 ? -2 : 1);
-              const int ni = axis == 0 ? i + o : i;
-              const int nj = axis == 1 ? j + o : j;
-              if (ni >= 0 && ni < f.nx && nj >= 0 && nj < f.ny) {
-                const bool before = axis == 0 ? (i_up ? ni < i : ni > i) : (j_up ? nj < j : nj > j);
-                const unsigned* a = plan.ver + nj * f.nx + ni;
-                if ((pass ? ld_acquire(a) : ld_relaxed(a)) < (unsigned)s + (before ? 1u : 0u)) ok = false;
-              }
-            }
-          }
-          if (!ok) {
-            if (*((volatile const int*)&err->code) != 0) break;
-            if (++polls > (1LL << 26)) {  // deadlock guard: fail loudly, never hang
-              tc::raise(err, E_ERROR, W_DEADLOCK, i, j, (double)s);
-              break;
-            }
-            if (plan.poll_ns) __nanosleep(plan.poll_ns);
-          }
-        }
-        if (!ok) break;
-      }
-    }
-    if (plan.split_wait)
-      gbar(g);
-    else
-      __syncthreads();
-    if (tr) plan.trace[item * 8 + 1] = gtimer();
-    unsigned long long* st = tr ? plan.trace + item * 8 + 4 : nullptr;
-    double* SB = smem + 12 * VEC + c;
-    double* RB = smem + 13 * VEC + c;
-    P4 cpv{};
-    int w;
-    if (has_rhs)
-      w = g < 2 ? face_split<M, ORDER, 0, true>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st)
-                : face_split<M, ORDER, 1, true>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st);
-    else
-      w = g < 2 ? face_split<M, ORDER, 0, false>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st)
-                : face_split<M, ORDER, 1, false>(f, ctx, g, q, valid, i, j, L, U, F, SB, &rhs, RB, &cpv, st);
-    if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, 0.0);
-    __syncthreads();
-    if (tr) plan.trace[item * 8 + 2] = gtimer();
-    w = W_NONE;
-    double bad = 0.0;
-    if (g == 0) {
-      w = update_split<M>(f, has_rhs ? &rhs : nullptr, ctx, q, valid, i, j, smem, &bad, cpv,
-                          valid ? f.dx[i] : 1.0, valid ? f.dy[j] : 1.0);
-      if (w && valid && q == 0) tc::raise(err, tc::code_for(w), w, i, j, bad);
-    }
-    __syncthreads();
-    if (tr) plan.trace[item * 8 + 3] = gtimer();
-    if (g == 0 && q == 0 && valid && w == W_NONE) st_release(plan.ver + j * f.nx + i, (unsigned)s + 1u);
-  }
 }
 
 }  // namespace sp

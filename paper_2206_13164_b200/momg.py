@@ -631,10 +631,10 @@ def cavity_context(M: int, space_order: int = 1, model: CollisionKind = Collisio
 
 
 def set_sweep_mode(mode: str) -> None:
-    """'persistent' (default: one dataflow kernel per fast_sweep_step; band
-    tasks at first order), 'items' (persistent wavefront items only), 'warp'
-    (persistent warp-per-cell kernels) or 'diag' (one launch per
+    """'persistent' (default: one dataflow kernel per fast_sweep_step; the band
+    kernels for M <= 5), 'warp' (the same without the band kernels:
+    thread-per-face / warp-per-cell) or 'diag' (one launch per
     anti-diagonal).  Results are identical up to rounding."""
-    rc = lib().momg_set_sweep_mode({"diag": 0, "persistent": 1, "warp": 2, "items": 3}[mode])
+    rc = lib().momg_set_sweep_mode({"diag": 0, "persistent": 1, "warp": 2}[mode])
     if rc:
         raise ValueError(mode)

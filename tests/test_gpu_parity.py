@@ -40,7 +40,7 @@ def rel_res(got, want):
     return float(np.max(np.abs(got - want) / scale))
 
 
-@pytest.fixture(params=["persistent", "items", "diag"])
+@pytest.fixture(params=["persistent", "warp", "diag"])
 def sweep_mode(request):
     momg.set_sweep_mode(request.param)
     yield request.param
