@@ -22,6 +22,7 @@
 #include "kernels_v3.cuh"
 #include "split_cell.cuh"
 #include "band_sweep.cuh"
+#include "transfer.cuh"
 #include "band2.h"
 
 namespace momg_gpu {
@@ -690,7 +691,25 @@ struct Launch {
       momg_rt::count_launch(nx + ny - 1);
     }
   }
+  static int xf_grid(int cells) {
+    const int need = (cells + xf::XT - 1) / xf::XT;
+    return need < 148 * 8 ? need : 148 * 8;
+  }
+  static void xf_attrs() {
+    if constexpr (use_split<M>()) {
+      static bool done = false;
+      if (done) return;
+      done = true;
+    }
+  }
   static void restrict_sol(const momg_field* fine, momg_field* coarse) {
+    if constexpr (use_split<M>()) {  // warp-staged records (transfer.cuh)
+      xf_attrs();
+      xf::xf_restrict_sol<M><<<xf_grid(coarse->nx * coarse->ny), xf::XT, 0, momg_rt::stream()>>>(
+          fine->dev(), coarse->dev(), momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     if constexpr (use_tc<M>()) {
       tc_attrs();
       tc::k3_restrict_sol<M><<<tc_grid(coarse->nx * coarse->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes,
@@ -704,6 +723,13 @@ struct Launch {
     momg_rt::count_launch(1);
   }
   static void restrict_res(const momg_field* arrays, const momg_field* coarse, momg_field* out) {
+    if constexpr (use_split<M>()) {
+      xf_attrs();
+      xf::xf_restrict_res<M><<<xf_grid(coarse->nx * coarse->ny), xf::XT, 0, momg_rt::stream()>>>(
+          arrays->dev(), coarse->dev(), out->dev(), momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     if constexpr (use_tc<M>()) {
       tc_attrs();
       tc::k3_restrict_res<M><<<tc_grid(coarse->nx * coarse->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes,
@@ -719,6 +745,13 @@ struct Launch {
     momg_rt::count_launch(1);
   }
   static void fas(momg_field* fine, const momg_field* before, const momg_field* after) {
+    if constexpr (use_split<M>()) {
+      xf_attrs();
+      xf::xf_fas<M><<<xf_grid(fine->nx * fine->ny), xf::XT, 0, momg_rt::stream()>>>(
+          fine->dev(), before->dev(), after->dev(), momg_rt::err_dev());
+      momg_rt::count_launch(1);
+      return;
+    }
     if constexpr (use_tc<M>()) {
       tc_attrs();
       tc::k3_fas<M><<<tc_grid(fine->nx * fine->ny, tc::VS), tc::VS, tc::TSmem<M>::bytes, momg_rt::stream()>>>(
