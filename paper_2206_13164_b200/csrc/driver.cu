@@ -188,6 +188,57 @@ static void nmg_cycle(Hierarchy& h, int level, momg_field* field, const momg_fie
   *work += 4 * cells * pol.s2;
 }
 
+// A solve iteration captured as a CUDA graph (first replay() captures it).
+// Capture needs a non-default stream; if the stream cannot be captured the
+// iteration simply runs eagerly (same kernels, same results).
+struct IterGraph {
+  cudaGraphExec_t exec = nullptr;
+  long long nodes = 0;
+  bool failed = false;
+  ~IterGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+  // 0: not run (the caller runs body eagerly), 1: captured and launched
+  // (body's host-side effects happened once), 2: replayed
+  template <class F>
+  int replay(F&& body, cudaStream_t st) {
+    if (failed || st == nullptr) return 0;
+    if (!exec) {
+      cudaGraph_t g = nullptr;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        failed = true;
+        cudaGetLastError();
+        return 0;
+      }
+      const long long l0 = momg_rt::launches();
+      try {
+        body();
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      const cudaError_t ec = cudaStreamEndCapture(st, &g);
+      nodes = momg_rt::launches() - l0;
+      momg_rt::count_launch(-nodes);  // counted per replay below
+      if (ec != cudaSuccess || !g || cudaGraphInstantiate(&exec, g, 0) != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        exec = nullptr;
+        failed = true;
+        cudaGetLastError();
+        return 0;
+      }
+      cudaGraphDestroy(g);
+      momg_rt::note_launch(cudaGraphLaunch(exec, st));
+      momg_rt::count_launch(nodes);
+      return 1;
+    }
+    momg_rt::note_launch(cudaGraphLaunch(exec, st));
+    momg_rt::count_launch(nodes);
+    return 2;
+  }
+};
+
 static double scalar(momg_err& e) {
   double v = 0.0;
   check(momg_gpu::fetch_scalar(&v, &e), e);
@@ -278,29 +329,47 @@ int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_
     momg_gpu::op_mass(field, 1.0);
     const double target = scalar(e);
     Cycle pol{opts->s1, opts->s2, opts->s3, opts->gamma};
+    // One iteration of the solve loop (multigrid.cpp:272-283): the smoother /
+    // cycle, mass_correction (its positivity check on the device), the
+    // residual and its norm -- all stream-ordered, one host read at the end.
+    // After the first (eager) iteration, which initialises every lazily
+    // allocated buffer and kernel attribute, the iteration is captured once
+    // as a CUDA graph and replayed: one launch per iteration instead of one
+    // per kernel.
+    long long iter_work = 0;
+    auto body = [&]() {
+      long long w0 = work;
+      if (opts->kind == 0) {
+        // euler_step(field, res, {}, ctx) with res = R(field) of the previous iteration
+        momg_gpu::op_global_dt(dctx, field);
+        momg_gpu::op_euler(field, res.f, nullptr);
+      } else if (opts->kind == 1) {
+        momg_gpu::op_sweep(dctx, field, nullptr, kCanon);
+        work += 4LL * field->nx * field->ny;
+      } else {
+        nmg_cycle(h, (int)h.grids.size() - 1, field, nullptr, dctx, pol, &work);
+      }
+      // mass_correction (single_level.cpp:176-183)
+      momg_gpu::op_mass(field, target);
+      momg_gpu::op_mass_guard();
+      momg_gpu::op_scale_by_factor(field);
+      momg_gpu::op_residual(dctx, field, res.f);
+      momg_gpu::op_norm(res.f, field);
+      iter_work = work - w0;
+    };
+    IterGraph graph;
     for (int n = 1; n <= cap; ++n) {
       int step_rc = MOMG_OK;
       std::string step_msg;
       try {
-        if (opts->kind == 0) {
-          // euler_step(field, res, {}, ctx) with res = R(field) of the previous iteration
-          momg_gpu::op_global_dt(dctx, field);
-          momg_gpu::op_euler(field, res.f, nullptr);
-        } else if (opts->kind == 1) {
-          momg_gpu::op_sweep(dctx, field, nullptr, kCanon);
-          work += 4LL * field->nx * field->ny;
-        } else {
-          nmg_cycle(h, (int)h.grids.size() - 1, field, nullptr, dctx, pol, &work);
+        const long long w_before = work;
+        const int how = n == 1 ? 0 : graph.replay(body, momg_rt::stream());
+        if (how == 0) {
+          work = w_before;  // (a failed capture ran body's host side only)
+          body();
+        } else if (how == 2) {
+          work += iter_work;
         }
-        // mass_correction (single_level.cpp:176-183)
-        momg_gpu::op_mass(field, target);
-        const double current = scalar(e);
-        if (!(current > 0.0) || !std::isfinite(current))
-          throw Fail(MOMG_NONPHYSICAL_STATE,
-                     "mass_correction: nonpositive total mass " + std::to_string(current));
-        momg_gpu::op_scale_by_factor(field);
-        momg_gpu::op_residual(dctx, field, res.f);
-        momg_gpu::op_norm(res.f, field);
         rep.final_norm = scalar(e);
       } catch (const Fail& f) {
         step_rc = f.code;

@@ -40,6 +40,20 @@ __global__ void k_negate(const double* __restrict__ src_c, const double* __restr
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < nparam; q += stride) dst_p[q] = src_p[q];
 }
 
+// mass_correction's check (single_level.cpp:176-183) on the device, so a
+// solve iteration needs no host round trip before the rescale: a nonpositive
+// or non-finite current mass is recorded as NonphysicalState and every later
+// kernel of the iteration early-exits
+__global__ void k_mass_guard(const double* current, DevErr* err) {
+  const double m = *current;
+  if (threadIdx.x == 0 && (!(m > 0.0) || !isfinite(m)) && atomicCAS(&err->code, 0, E_NONPHYSICAL) == 0) {
+    err->what = W_MASS;
+    err->i = err->j = -1;
+    err->value = m;
+    __threadfence();
+  }
+}
+
 __global__ void k_scale(double* c, size_t n, const double* factor_dev, const DevErr* err) {
   if (err_set(err)) return;
   const double f = *factor_dev;
@@ -262,6 +276,7 @@ static const char* what_text(int w) {
     case W_RESTRICT: return "restrict_solution: nonphysical coarse state";
     case W_ES_UNSUPPORTED: return "ES-BGK collision is not available on the device path";
     case W_DEADLOCK: return "persistent sweep: dependency wait timed out (internal error)";
+    case W_MASS: return "mass_correction: nonpositive total mass";
     default: return "unknown failure";
   }
 }
@@ -545,6 +560,10 @@ void op_mass(const momg_field* f, double target) {
   k_final<<<1, 1024, 0, momg_rt::stream()>>>(momg_rt::red_buf(), RED_BLOCKS, 0, target,
                                              momg_rt::red_buf() + RED_BLOCKS);
   momg_rt::count_launch(2);
+}
+void op_mass_guard() {
+  k_mass_guard<<<1, 32, 0, momg_rt::stream()>>>(momg_rt::red_buf() + RED_BLOCKS, momg_rt::err_dev());
+  momg_rt::count_launch(1);
 }
 void op_scale_by_factor(momg_field* f) {
   const size_t n = (size_t)f->nx * f->ny * f->NP;

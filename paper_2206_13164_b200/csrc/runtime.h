@@ -104,6 +104,8 @@ void op_axpy(momg_field* dst, const momg_field* src);
 void op_copy(momg_field* dst, const momg_field* src);
 void op_mass(const momg_field* f, double target);
 void op_scale_by_factor(momg_field* f);
+// device-side check of the mass op_mass left (NonphysicalState when <= 0)
+void op_mass_guard();
 void op_norm(const momg_field* res, const momg_field* field);
 void op_rscale(const DevCtx& ctx, const momg_field* f);
 // global_dt (single_level.cpp:31-38): min local_dt, result left on the device

@@ -47,6 +47,7 @@ enum : int {
   W_RESTRICT = 13,     // restrict_solution: nonphysical coarse state
   W_ES_UNSUPPORTED = 14,
   W_DEADLOCK = 15,     // persistent sweep: dependency wait timed out (bug guard)
+  W_MASS = 16,         // mass_correction: nonpositive / non-finite total mass
 };
 
 // Problem constants (SolveContext, single_level.hpp:27-34), by value per launch.
