@@ -223,6 +223,8 @@ int momg_debug_trace(long long cap);
 long long momg_debug_trace_read(unsigned long long* host, long long n);
 /* number of kernels this library has launched since load (gpu_launches) */
 long long momg_launch_count(void);
+/* solve_steady iterations replayed from a captured CUDA graph since load */
+long long momg_graph_replays(void);
 
 #ifdef __cplusplus
 }

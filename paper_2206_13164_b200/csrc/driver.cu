@@ -191,6 +191,7 @@ static void nmg_cycle(Hierarchy& h, int level, momg_field* field, const momg_fie
 // A solve iteration captured as a CUDA graph (first replay() captures it).
 // Capture needs a non-default stream; if the stream cannot be captured the
 // iteration simply runs eagerly (same kernels, same results).
+static long long g_graph_replays = 0;
 struct IterGraph {
   cudaGraphExec_t exec = nullptr;
   long long nodes = 0;
@@ -235,6 +236,7 @@ struct IterGraph {
     }
     momg_rt::note_launch(cudaGraphLaunch(exec, st));
     momg_rt::count_launch(nodes);
+    ++g_graph_replays;
     return 2;
   }
 };
@@ -259,6 +261,8 @@ static int map_fail(const Fail& f, momg_err* err) {
 }
 
 extern "C" {
+
+long long momg_graph_replays(void) { return g_graph_replays; }
 
 int momg_nmg_cycle(const momg_ctx* ctx, momg_field* field, int levels, int s1, int s2, int s3,
                    int gamma, long long* work, momg_err* err) {

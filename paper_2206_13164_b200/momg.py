@@ -129,6 +129,7 @@ def lib() -> C.CDLL:
         L.momg_version.restype = C.c_char_p
         L.momg_get_stream.restype = C.c_void_p
         L.momg_launch_count.restype = C.c_longlong
+        L.momg_graph_replays.restype = C.c_longlong
         _lib = L
     return _lib
 
@@ -615,6 +616,11 @@ def synchronize() -> None:
 
 def launch_count() -> int:
     return lib().momg_launch_count()
+
+
+def graph_replays() -> int:
+    """solve_steady iterations replayed from a captured CUDA graph since load."""
+    return lib().momg_graph_replays()
 
 
 def cavity_context(M: int, space_order: int = 1, model: CollisionKind = CollisionKind.bgk,

@@ -292,9 +292,15 @@ def test_solve_steady_parity(solver, nx, levels):
     assert wr["converged"]
     f = momg.CellField.from_host(mgrid(g), M, c, p)
     opts = momg.SolverOptions(momg.SolverKind(kind), 1e-8, 0, levels)
+    replays = momg.graph_replays()
+    launches = momg.launch_count()
     rep = momg.solve_steady(f, mctx(octx), opts)
     assert rep.converged
     assert abs(rep.iterations - wr["iterations"]) <= 1
+    # iterations 2.. are replays of the captured iteration graph; the launch
+    # counter still counts every kernel of every iteration
+    assert momg.graph_replays() - replays == rep.iterations - 2
+    assert momg.launch_count() - launches >= 3 * rep.iterations
     gc, gp = f.download()
     mg, mw = macro(gc, gp), macro(wc, wp)
     assert np.max(np.abs(mg - mw)) <= 1e-8 * np.max(np.abs(mw))
