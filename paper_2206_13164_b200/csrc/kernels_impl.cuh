@@ -471,7 +471,7 @@ struct Launch {
   // the fused path does not apply (the caller runs the two operations).
   static bool sweep_res(const DevCtx& ctx, momg_field* f, const int* order, momg_field* out, int iters) {
     if constexpr (use_split<M>()) {
-      if (ctx.order == 1 && iters >= 1 && iters <= 4 && band_sweep_enabled()) {
+      if (ctx.order == 1 && iters >= 1 && iters <= 4 && band_sweep_enabled() && ctx.collision != 1) {
         static bool battr = false;
         if (!battr) {
           set_smem(sp::k5_band<M, 32>, sp::BandLayout<M>::bytes);
@@ -511,7 +511,7 @@ struct Launch {
   }
   static void residual(const DevCtx& ctx, const momg_field* f, momg_field* out) {
     if constexpr (use_split<M>()) {
-      if (ctx.order == 1 && band_sweep_enabled()) {
+      if (ctx.order == 1 && band_sweep_enabled() && ctx.collision != 1) {
         // the band kernel in residual mode: (band, diagonal chunk) tasks
         static bool rattr = false;
         if (!rattr) {
@@ -563,7 +563,7 @@ struct Launch {
   // persistent kernel runs them as one launch so the sweeps overlap)
   static void sweep_n(const DevCtx& ctx, momg_field* f, const momg_field* rhs, const int* order, int iters) {
     if constexpr (use_split<M>()) {
-      if (!band_sweep_enabled() || iters > 4) {
+      if (!band_sweep_enabled() || ctx.collision == 1 || iters > 4) {
         for (int it = 0; it < iters; ++it) sweep1(ctx, f, rhs, order, 1);
         return;
       }
@@ -582,7 +582,8 @@ struct Launch {
       DevErr* err = momg_rt::err_dev();
       DevCtx c = ctx;
       if constexpr (use_split<M>()) {
-        if (band_sweep_enabled()) {
+        // the band kernels (BGK / Shakhov); ES-BGK runs the thread-per-face kernels
+        if (band_sweep_enabled() && ctx.collision != 1) {
           if (ctx.order == 1 && !rhs) {
             static bool battr = false;
             if (!battr) {
@@ -802,7 +803,7 @@ struct Launch {
   // this process's strips; first order, M <= 5)
   static bool strips_sweep_res(const DevCtx& ctx, const StripLaunch& L) {
     if constexpr (use_split<M>()) {
-      if (ctx.order != 1) return false;
+      if (ctx.order != 1 || ctx.collision == 1) return false;
       static bool battr = false;
       if (!battr) {
         set_smem(sp::k5_band<M, 32, false, true>, sp::BandLayout<M>::bytes);

@@ -32,6 +32,7 @@ __device__ __forceinline__ int code_for(int what) {
     case W_DT_HALVING:
     case W_FAS: return E_SOLVER;
     case W_ES_UNSUPPORTED: return E_CONFIG;
+    case W_NON_SPD: return E_NONSPD;
     default: return E_NONPHYSICAL;
   }
 }
@@ -75,10 +76,11 @@ __global__ void __launch_bounds__(VS) k3_residual(DevField f, DevField out, DevC
       double nu, q[3];
       const int w = collision_scalars<M>(S, cp, ctx, &nu, q);
       if (w) {
-        raise(err, code_for(w), w, i, j, 0.0);
+        raise(err, code_for(w), w, i, j, w == W_NON_SPD ? q[0] : 0.0);
       } else {
         assemble<M>(S, nu, q, ctx.collision == 2, ctx.shakhov_w, base + tid, base + 16 + tid,
-                    base + 32 + tid, base + 48 + tid, f.dx[i], f.dy[j], nullptr, D);
+                    base + 32 + tid, base + 48 + tid, f.dx[i], f.dy[j], nullptr, D, ctx.collision == 1, cp.v[3],
+                    ctx.prandtl);
         store_vec<M>(D, out.c + (size_t)cell * NP);
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) out.p[(size_t)cell * 4 + q4] = cp.v[q4];
@@ -111,14 +113,18 @@ __device__ __forceinline__ int update_cell(const DevField& f, const DevField* rh
   const double dt = ctx.cfl / ((fabs(cp.v[0]) + cc) / f.dx[i] + (fabs(cp.v[1]) + cc) / f.dy[j]);
   double nu, q[3];
   int w = collision_scalars<M>(S, cp, ctx, &nu, q);
-  if (w) return w;
+  if (w) {
+    if (w == W_NON_SPD) *bad = q[0];
+    return w;
+  }
   if (rhs) {
     load_vec<M, CG>(rhs->c + cell * NP, R);
     const P4 rp = ldp<CG>(rhs->p + cell * 4);
     project<M>(R, rp, cp);
   }
   assemble<M>(S, nu, q, ctx.collision == 2, ctx.shakhov_w, base + tid, base + 16 + tid,
-              base + 32 + tid, base + 48 + tid, f.dx[i], f.dy[j], rhs ? R : nullptr, D);
+              base + 32 + tid, base + 48 + tid, f.dx[i], f.dy[j], rhs ? R : nullptr, D, ctx.collision == 1,
+              cp.v[3], ctx.prandtl);
   for (int attempt = 0; attempt < 2; ++attempt) {
     const double step = attempt == 0 ? dt : 0.5 * dt;
 #pragma unroll

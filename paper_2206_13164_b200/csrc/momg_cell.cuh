@@ -4,6 +4,7 @@
 // buffers (WarpBuf), descriptors in the block header (BlockHdr).
 #pragma once
 
+#include "es_bgk.cuh"
 #include "momg_device.cuh"
 
 namespace momg_gpu {
@@ -101,6 +102,7 @@ __device__ __forceinline__ int code_of(int what) {
     case W_DT_HALVING:
     case W_FAS: return E_SOLVER;
     case W_ES_UNSUPPORTED: return E_CONFIG;
+    case W_NON_SPD: return E_NONSPD;
     default: return E_NONPHYSICAL;
   }
 }
@@ -255,12 +257,20 @@ __device__ __forceinline__ int grad_normalize(const uint32_t* tab, WarpBuf<M, OR
 // registers.
 template <int M>
 __device__ __forceinline__ int collision(const uint32_t* tab, const double* S, const double* cp,
-                                         const DevCtx* ctx, double* Q) {
+                                         const DevCtx* ctx, double* Q, double* scratch) {
   const double rho = S[0];
   if (!(rho > 0.0)) return W_MACRO_RHO;
   const double theta = cp[3];
   if (!(theta > 0.0)) return W_MACRO_RHO;  // maxwellian_rep precondition
-  if (ctx->collision == 1) return W_ES_UNSUPPORTED;
+  const bool es_bgk = ctx->collision == 1;
+  if (es_bgk) {
+    // ES-BGK: the Gaussian equilibrium (es_bgk.cuh) built once by lane 0 in
+    // the warp's scratch vector, flat coefficient order
+    double bad = 0.0;
+    if (es::check<1>(S, theta, ctx->prandtl, &bad)) return W_NON_SPD;
+    if (lane_id() == 0) es::fill<M, 1>(S, theta, ctx->prandtl, scratch);
+    __syncwarp();
+  }
   const double nu = ctx->nu_coef * rho * pow(theta, ctx->nu_exp);
   double q[3] = {0.0, 0.0, 0.0};
   const bool shakhov = ctx->collision == 2;
@@ -275,6 +285,7 @@ __device__ __forceinline__ int collision(const uint32_t* tab, const double* S, c
   for (int t = 0; t < Cfg<M>::T; ++t) {
     const int k = lane + 32 * t;
     double eq = k == 0 ? rho : 0.0;
+    if (es_bgk && k < Cfg<M>::N) eq = scratch[item_pos<M>(t)];
     if (shakhov) {
       const uint32_t ms = misc<M>(tab, t);
       const int a1 = byte_of(ms, 0), a2 = byte_of(ms, 1), a3 = byte_of(ms, 2);
@@ -411,7 +422,7 @@ template <int M, int ORDER>
 __device__ __forceinline__ int cell_residual(const DevField* f, const DevCtx* ctx, const uint32_t* tab,
                                              int i, int j, WarpBuf<M, ORDER>& sb, double* R) {
   constexpr int T = Cfg<M>::T;
-  int w = collision<M>(tab, sb.cell[0], sb.cp[0], ctx, R);
+  int w = collision<M>(tab, sb.cell[0], sb.cp[0], ctx, R, sb.X1);
   if (w) return w;
   double Fp[T], Fm[T];
   if ((w = cell_face<M, ORDER>(f, ctx, tab, i, j, 0, true, sb, Fp))) return w;

@@ -277,6 +277,7 @@ static const char* what_text(int w) {
     case W_ES_UNSUPPORTED: return "ES-BGK collision is not available on the device path";
     case W_DEADLOCK: return "persistent sweep: dependency wait timed out (internal error)";
     case W_MASS: return "mass_correction: nonpositive total mass";
+    case W_NON_SPD: return "equilibrium_rep: anisotropic-Gaussian tensor not SPD";
     default: return "unknown failure";
   }
 }

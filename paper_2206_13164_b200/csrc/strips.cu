@@ -218,7 +218,7 @@ int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const i
   for (int k = 0; k < 4; ++k) L.order[k] = (sweep_order ? sweep_order : canon)[k];
   s->epoch += 4;  // every rank advances identically, launched or not
   if (!momg_gpu::ops_for(s->M)->strips_sweep_res(momg_gpu::make_ctx(ctx), L))
-    return fail(err, MOMG_CONFIG, "momg_strips_fast_sweep_residual: strips run first order, M <= 5");
+    return fail(err, MOMG_CONFIG, "momg_strips_fast_sweep_residual: strips run first order, M <= 5, BGK / Shakhov");
   const int rc = momg_rt::sync_check(err);
   if (rc == MOMG_OK && evals) *evals += 4LL * (s->b[s->last + 1] - s->b[s->first]) * s->ny;
   return rc;

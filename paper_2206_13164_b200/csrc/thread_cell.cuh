@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "es_bgk.cuh"
 #include "gen/simplex_gen.cuh"
 #include "types.h"
 
@@ -379,9 +380,12 @@ __device__ __forceinline__ int collision_scalars(const double* S, const P4& cp, 
   const double rho = S[0];
   if (!(rho > 0.0)) return W_MACRO_RHO;
   if (!(cp.v[3] > 0.0)) return W_MACRO_RHO;
-  if (ctx.collision == 1) return W_ES_UNSUPPORTED;
-  *nu = ctx.nu_coef * rho * pow(cp.v[3], ctx.nu_exp);
   q[0] = q[1] = q[2] = 0.0;
+  if (ctx.collision == 1) {  // ES-BGK: SPD check here, the Gaussian in assemble (min eig -> q[0])
+    const int w = es::check<VS>(S, cp.v[3], ctx.prandtl, &q[0]);
+    if (w) return w;
+  }
+  *nu = ctx.nu_coef * rho * pow(cp.v[3], ctx.nu_exp);
   if (ctx.collision == 2) {
     q[0] = 2.0 * S[flat3(3, 0, 0) * VS] + S[flat3(3, 0, 0) * VS] + S[flat3(1, 2, 0) * VS] + S[flat3(1, 0, 2) * VS];
     q[1] = 2.0 * S[flat3(0, 3, 0) * VS] + S[flat3(2, 1, 0) * VS] + S[flat3(0, 3, 0) * VS] + S[flat3(0, 1, 2) * VS];
@@ -392,11 +396,15 @@ __device__ __forceinline__ int collision_scalars(const double* S, const P4& cp, 
 
 // Writes into D (thread vector): D_k = Q_k - (Fxp-Fxm)/dx - (Fyp-Fym)/dy
 // (cell_residual assembly, spatial.cpp:127-132) [- rhs_k], Q = nu (eq - S).
+// ES-BGK (es, basis temperature theta): the Gaussian equilibrium is first
+// written into D (es::fill) and read back element by element.
 template <int M>
 __device__ __forceinline__ void assemble(const double* S, double nu, const double* q, int shakhov,
                                          double shw, const double* Fxm, const double* Fxp,
                                          const double* Fym, const double* Fyp, double dx, double dy,
-                                         const double* rhs, double* D) {
+                                         const double* rhs, double* D, int es = 0, double theta = 1.0,
+                                         double prandtl = 1.0) {
+  if (es) es::fill<M, VS>(S, theta, prandtl, D);
   double eq[Gen<M>::N];
 #pragma unroll
   for (int k = 0; k < Gen<M>::N; ++k) eq[k] = 0.0;
@@ -411,7 +419,7 @@ __device__ __forceinline__ void assemble(const double* S, double nu, const doubl
   }
 #pragma unroll
   for (int k = 0; k < Gen<M>::N; ++k) {
-    double r = nu * (eq[k] - S[k * VS]);
+    double r = nu * ((es ? D[k * VS] : eq[k]) - S[k * VS]);
     r -= (Fxp[k * VS] - Fxm[k * VS]) / dx;
     r -= (Fyp[k * VS] - Fym[k * VS]) / dy;
     if (rhs) r -= rhs[k * VS];

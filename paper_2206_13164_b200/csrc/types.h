@@ -48,6 +48,7 @@ enum : int {
   W_ES_UNSUPPORTED = 14,
   W_DEADLOCK = 15,     // persistent sweep: dependency wait timed out (bug guard)
   W_MASS = 16,         // mass_correction: nonpositive / non-finite total mass
+  W_NON_SPD = 17,      // equilibrium_rep: ES-BGK tensor not SPD (NonSpdTensor)
 };
 
 // Problem constants (SolveContext, single_level.hpp:27-34), by value per launch.
