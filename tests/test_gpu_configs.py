@@ -124,3 +124,45 @@ def test_grad_normalize_cap(M):
         momg.restrict_solution(fine, mgrid(cg))
         momg.synchronize()
     assert type(ge.value) is momg.Error
+
+
+@pytest.mark.parametrize("name,cap", [("C3", 200), ("C4", 200)])
+def test_config_residual_history(name, cap):
+    """The residual-ratio history of the whole solve_steady loop against the
+    oracle's run of the same config (as far as the oracle has got: C3 /
+    C4 V-cycles take 2.5 / 4.7 min each on one core), at 1e-9 relative per
+    iteration; when the oracle's run has ended (converged, or C4's
+    SolverError -> NonConvergence), the device must end the same way at the
+    same iteration."""
+    import json
+    h = json.load(open(os.path.join(GOLD, f"{name}_history.json")))
+    want = h["ratios"][:cap]
+    n, M, order, model, kn, pr, lid, bt, levels = CONFIGS[name]
+    octx = cavity_ctx(M, order, model, kn=kn, lid=lid, prandtl=pr, bottom_theta=bt)
+    octx.c_bound = octx.cfl_c_bound = float(h["c_bound"])
+    g = momg.Grid2D.uniform(n, n)
+    f = momg.uniform_field(g, M, 1.0, (0.0, 0.0, 0.0), 1.0)
+    ended = (h["converged"] or h["error"]) and len(h["ratios"]) <= cap
+    opts = momg.SolverOptions(momg.SolverKind.nmg, 1e-8, 0 if ended else len(want), levels)
+    try:
+        rep = momg.solve_steady(f, mctx(octx), opts)
+        outcome = "converged"
+    except momg.NonConvergence as e:
+        rep, outcome = e.report, str(e)
+    got = rep.history[:len(want)]
+    assert len(got) == len(want) or (ended and abs(len(got) - len(want)) <= 1)
+    for it, (a, b) in enumerate(zip(got, want)):
+        assert abs(a - b) <= 1e-9 * b, f"iteration {it + 1}: {a} vs {b}"
+    if ended:
+        if h["converged"]:
+            assert outcome == "converged" and abs(rep.iterations - len(h["ratios"])) <= 1
+            # converged macroscopic fields at 1e-8 (the oracle's compact fixture)
+            z = np.load(os.path.join(GOLD, f"{name}_final.npz"))
+            c, p = f.download()
+            c3 = c.reshape(n, n, -1)
+            for got_s, want_s in ((c3[:, :, :20].sum(axis=1), z["row_sums"]), (c3[:, :, :20].sum(axis=0), z["col_sums"])):
+                assert np.max(np.abs(got_s - want_s)) <= 1e-8 * np.max(np.abs(want_s))
+            assert np.max(np.abs(p.reshape(n, n, 4)[::8, ::8] - z["params_sub"])) <= 1e-8 * np.max(np.abs(z["params_sub"]))
+        else:
+            assert "step failed" in outcome or "nonphysical" in outcome, outcome
+            assert abs(rep.iterations - len(h["ratios"])) <= 1

@@ -40,6 +40,12 @@ def main():
     for name in sys.argv[1:]:
         hist = json.load(open(os.path.join(RUNS, f"{name}_port_hist.json")))
         n = hist["config"]["n"]
+        # residual-ratio history of the oracle's solve_steady loop (and how it ended)
+        hout = os.path.join(ROOT, "tests", "golden", f"{name}_history.json")
+        json.dump(dict(ratios=[h["ratio"] for h in hist["history"]], r0_norm=hist["r0_norm"],
+                       converged=bool(hist.get("converged", False)), error=hist.get("error"),
+                       c_bound=hist["config"]["c_bound"]), open(hout, "w"), indent=0)
+        print(hout)
         for tag in ("it1", "it2", "final"):
             path = os.path.join(RUNS, f"{name}_port_{tag}.npz")
             if not os.path.exists(path):
