@@ -171,11 +171,18 @@ int momg_residual_scale(const momg_ctx* ctx, const momg_field* field, double* ou
 int momg_defect(const momg_field* res, const momg_field* rhs, momg_field* out, momg_err* err);
 /* coarse_rhs += coarse_res (multigrid.cpp:192-193): dst.coeffs += src.coeffs */
 int momg_axpy(momg_field* dst, const momg_field* src, momg_err* err);
+/* f.coeffs *= factor: mass_correction's rescale (single_level.cpp:176-183) with the
+   factor target / total mass computed by the caller (strips of a partitioned level) */
+int momg_field_scale(momg_field* f, double factor, momg_err* err);
 
 /* ---- the host driver (kept as host C++, multigrid.cpp:44-65, 166-320) --- */
 /* nmg_cycle on the hierarchy GridHierarchy::build(field grid, levels) */
 int momg_nmg_cycle(const momg_ctx* ctx, momg_field* field, int levels, int s1, int s2, int s3,
                    int gamma, long long* work, momg_err* err);
+/* nmg_cycle for R(f) = rhs (rhs nullable) on GridHierarchy::build(field grid, levels):
+   the coarse problem of a cycle whose finer level runs elsewhere (strips) */
+int momg_nmg_cycle_rhs(const momg_ctx* ctx, momg_field* field, const momg_field* rhs, int levels, int s1,
+                       int s2, int s3, int gamma, long long* work, momg_err* err);
 /* solve_steady: NonConvergence -> MOMG_NONCONVERGENCE with the partial report */
 int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_opts* opts,
                       momg_report* report, momg_err* err);
@@ -208,6 +215,19 @@ int momg_strips_import(momg_strips* s, int r, const void* handle, momg_err* err)
    C5 step); evals += the owned strips' cell updates */
 int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const int* sweep_order,
                                     long long* evals, momg_err* err);
+/* `iters` (<= 4) consecutive fast_sweep_step calls (no rhs) over the partition,
+   first or second order: one band launch */
+int momg_strips_fast_sweep(const momg_ctx* ctx, momg_strips* s, const int* sweep_order, int iters,
+                           long long* evals, momg_err* err);
+/* residual (spatial.cpp:135-159) of the owned strips into their residual fields:
+   each strip plus its neighbours' 1 (first order) or 2 (second order) columns,
+   copied from peer memory, then the single-field residual on that */
+int momg_strips_residual(const momg_ctx* ctx, momg_strips* s, momg_err* err);
+/* every strip's field (which = 0) or residual field (1) -> a full-level field
+   (own and peer memory): the agglomeration of a level on every rank */
+int momg_strips_gather(momg_strips* s, int which, momg_field* full, momg_err* err);
+/* the owned strips' columns of a full-level field -> their fields (0) / residual fields (1) */
+int momg_strips_scatter(momg_strips* s, int which, const momg_field* full, momg_err* err);
 
 /* ---- execution strategy of fast_sweep (same results either way) -------- */
 /* 1 (default): one persistent dataflow kernel per call (the band kernels for

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include "strips.h"
 #include "types.h"
 
 namespace momg_gpu {
@@ -18,6 +19,11 @@ struct Band2Plan {
   int has_rhs;
   int poll_ns;
   unsigned jitter;  // schedule perturbation seed (race stress tests; 0 = off)
+  // strip partition (the k5 BandPlan fields of the same names; no rhs)
+  const StripTab* strips;
+  unsigned epoch;
+  int kb_up, kb_dn, nk;
+  int sys;
 };
 }  // namespace sp
 struct DevCtx;
@@ -27,4 +33,11 @@ void band2_launch_m4(const DevField& f, const DevField& rhs, const DevCtx& ctx, 
                      const sp::Band2Plan& plan, cudaStream_t st);
 void band2_launch_m5(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err,
                      const sp::Band2Plan& plan, cudaStream_t st);
+// the strip-partition variant (plan.strips set, no rhs)
+void band2_strips_launch_m3(const DevField& geo, const DevCtx& ctx, DevErr* err, const sp::Band2Plan& plan,
+                            cudaStream_t st);
+void band2_strips_launch_m4(const DevField& geo, const DevCtx& ctx, DevErr* err, const sp::Band2Plan& plan,
+                            cudaStream_t st);
+void band2_strips_launch_m5(const DevField& geo, const DevCtx& ctx, DevErr* err, const sp::Band2Plan& plan,
+                            cudaStream_t st);
 }  // namespace momg_gpu

@@ -8,4 +8,8 @@ void band2_launch_m4(const DevField& f, const DevField& rhs, const DevCtx& ctx, 
                      const sp::Band2Plan& plan, cudaStream_t st) {
   band2_launch_impl<4>(f, rhs, ctx, err, plan, st);
 }
+void band2_strips_launch_m4(const DevField& geo, const DevCtx& ctx, DevErr* err, const sp::Band2Plan& plan,
+                            cudaStream_t st) {
+  band2_strips_launch_impl<4>(geo, ctx, err, plan, st);
+}
 }  // namespace momg_gpu

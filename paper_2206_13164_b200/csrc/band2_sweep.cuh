@@ -155,7 +155,7 @@ __device__ __forceinline__ int b2_update(const DevCtx& ctx, int q, bool valid, b
   return (valid && !good && fail == W_NONE) ? W_DT_HALVING : fail;
 }
 
-template <int M>
+template <int M, bool ST = false>
 __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf, DevCtx ctx, DevErr* err,
                                                       Band2Plan plan) {
   extern __shared__ __align__(128) double smem[];
@@ -165,9 +165,12 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
   constexpr int VEC = LY::VEC;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, g = warp / P, q = warp % P, c = tid & 31;
-  const int ntasks = plan.nsweeps * plan.nbands;
-  const CellAddr<> fa{nullptr, f.c, f.p, plan.ver}, ra{nullptr, rhsf.c, rhsf.p, plan.ver};
-  const bool has_rhs = plan.has_rhs != 0;
+  const int ntasks = plan.nsweeps * plan.nk;
+  const CellAddr<ST> fa{plan.strips, f.c, f.p, plan.ver};
+  const CellAddr<> ra{nullptr, rhsf.c, rhsf.p, plan.ver};
+  const unsigned ep = plan.epoch;  // counters count from here (0: zeroed per launch)
+  const bool sys = ST && plan.sys != 0;
+  const bool has_rhs = !ST && plan.has_rhs != 0;
   const bool o2 = plan.order == 2;
   for (;;) {
     if (tid == 0) {
@@ -178,27 +181,30 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
     __syncthreads();
     const int task = s_task;
     if (task >= ntasks || s_stop) return;
-    const int s = task / plan.nbands, k = task % plan.nbands;
+    const int s = task / plan.nk;
     const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
-    BandGeo<> b;
+    const int k = (dir == 0 || dir == 3 ? plan.kb_up : plan.kb_dn) + task % plan.nk;
+    BandGeo<ST> b;
     b.nx = f.nx;
     b.ny = f.ny;
     b.k = k;
     b.bw = B2W;
     b.i_up = dir == 0 || dir == 3;  // kSweepDirs (single_level.cpp:116-117)
     b.j_up = dir == 0 || dir == 1;
+    b.st = plan.strips;
+    b.strips_init();
     const int ir = B2W * k + c;
     const int dfirst = B2W * k, dlast = min(B2W * k + B2W - 1, f.nx - 1) + f.ny - 1;
     // ---- prologue: old states of dfirst .. dfirst+2, band k-1's new states
     // of dfirst-1 and dfirst-2, the rhs of dfirst; then the update scalars
 #pragma unroll 1
     for (int t = 0; t < 3; ++t)
-      band_load<M, 2>(fa, b, dfirst + t, 0, 18, (unsigned)s, b2_old<M>(smem, dfirst + t) + 2, SPV,
-                      b2_oldp<M>(smem, dfirst + t) + 8, warp, 16, err, kPrologueSleepNs);
+      band_load<M, 2>(fa, b, dfirst + t, 0, 18, ep + (unsigned)s, b2_old<M>(smem, dfirst + t) + 2, SPV,
+                      b2_oldp<M>(smem, dfirst + t) + 8, warp, 16, err, kPrologueSleepNs, 0u, sys);
     if (k > 0 && warp >= 14)
-      band_load<M, 2>(fa, b, dfirst - 1 - (warp - 14), -2, 2, (unsigned)s + 1u,
+      band_load<M, 2>(fa, b, dfirst - 1 - (warp - 14), -2, 2, ep + (unsigned)s + 1u,
                       b2_new<M>(smem, dfirst - 1 - (warp - 14)), SPV, b2_newp<M>(smem, dfirst - 1 - (warp - 14)),
-                      0, 1, err, kPrologueSleepNs);
+                      0, 1, err, kPrologueSleepNs, 0u, sys);
     if (has_rhs)
       band_load<M, 1>(ra, b, dfirst, 0, B2W, 0u, smem + (LY::V_RHS + (dfirst & 1)) * VEC, SPV,
                       smem + LY::PR + (dfirst & 1) * 64, warp, 16, err, 0);
@@ -341,11 +347,11 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
         if (wi == 0 && d > dfirst && c < B2W) {
           sched_jitter(plan.jitter, (unsigned)d);
           const int cl = b.cell(c, d - 1);
-          if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
+          if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, sys);
         }
         if (wi < 6 && d + 1 <= dlast)
-          band_load<M, 3>(fa, b, d + 3, 0, 18, (unsigned)s, b2_old<M>(smem, d + 3) + 2, SPV,
-                          b2_oldp<M>(smem, d + 3) + 8, wi, 6, err, plan.poll_ns, plan.jitter);
+          band_load<M, 3>(fa, b, d + 3, 0, 18, ep + (unsigned)s, b2_old<M>(smem, d + 3) + 2, SPV,
+                          b2_oldp<M>(smem, d + 3) + 8, wi, 6, err, plan.poll_ns, plan.jitter, sys);
         if (has_rhs && wi >= 6 && wi < 10 && d + 1 <= dlast)
           band_load<M, 4>(ra, b, d + 1, 0, B2W, 0u, smem + (LY::V_RHS + ((d + 1) & 1)) * VEC, SPV,
                           smem + LY::PR + ((d + 1) & 1) * 64, wi - 6, 4, err, 0);
@@ -353,8 +359,8 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
           band_pre<M, B2W>(f, ctx, b, d + 1, b2_old<M>(smem, d + 1) + 2, b2_oldp<M>(smem, d + 1) + 8,
                            smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         if (k > 0 && wi == 11 && d + 1 <= dlast)
-          band_load<M, 2>(fa, b, d, -2, 2, (unsigned)s + 1u, b2_new<M>(smem, d), SPV, b2_newp<M>(smem, d),
-                          0, 1, err, plan.poll_ns, plan.jitter);
+          band_load<M, 2>(fa, b, d, -2, 2, ep + (unsigned)s + 1u, b2_new<M>(smem, d), SPV, b2_newp<M>(smem, d),
+                          0, 1, err, plan.poll_ns, plan.jitter, sys);
         if (tid == 128) s_stop = stop_now;
       }
       __syncthreads();
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
     __syncthreads();
     if (warp == 4 && c < B2W) {
       const int cl = b.cell(c, dlast);
-      if (cl >= 0) st_release(plan.ver + cl, (unsigned)s + 1u);
+      if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, sys);
     }
   }
 }
@@ -384,8 +390,23 @@ void band2_launch_impl(const DevField& f, const DevField& rhs, const DevCtx& ctx
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   int nb = nsm;  // one CTA per SM (smem-bound); tasks are claimed dynamically
-  if (nb > plan.nsweeps * plan.nbands) nb = plan.nsweeps * plan.nbands;
+  if (nb > plan.nsweeps * plan.nk) nb = plan.nsweeps * plan.nk;
   sp::k6_band<M><<<nb, sp::THREADS, sp::Band2Layout<M>::bytes, st>>>(f, rhs, ctx, err, plan);
+}
+template <int M>
+void band2_strips_launch_impl(const DevField& geo, const DevCtx& ctx, DevErr* err, const sp::Band2Plan& plan,
+                              cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) {
+    cudaFuncSetAttribute(sp::k6_band<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sp::Band2Layout<M>::bytes);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int nb = nsm;
+  if (nb > plan.nsweeps * plan.nk) nb = plan.nsweeps * plan.nk;
+  sp::k6_band<M, true><<<nb, sp::THREADS, sp::Band2Layout<M>::bytes, st>>>(geo, geo, ctx, err, plan);
 }
 
 }  // namespace momg_gpu

@@ -287,6 +287,32 @@ int momg_nmg_cycle(const momg_ctx* ctx, momg_field* field, int levels, int s1, i
   }
 }
 
+// nmg_cycle with a right-hand side (the coarse problem of an outer cycle run
+// elsewhere, e.g. the strip-partitioned finest level of strips.py)
+int momg_nmg_cycle_rhs(const momg_ctx* ctx, momg_field* field, const momg_field* rhs, int levels, int s1, int s2,
+                       int s3, int gamma, long long* work, momg_err* err) {
+  if (err) err->code = 0;
+  if (int rc = momg_rt::ensure(err)) return rc;
+  if (!ctx || !field || (rhs && (rhs->nx != field->nx || rhs->ny != field->ny || rhs->M != field->M))) {
+    if (err) err->code = MOMG_ERR_ARG;
+    return MOMG_ERR_ARG;
+  }
+  momg_rt::acquire(field);
+  momg_rt::acquire(rhs);
+  try {
+    Hierarchy h = prepare(field, levels);
+    Cycle pol{s1, s2, s3, gamma};
+    long long w = 0;
+    nmg_cycle(h, (int)h.grids.size() - 1, field, rhs, momg_gpu::make_ctx(ctx), pol, &w);
+    momg_err e{};
+    check(momg_rt::sync_check(&e), e);
+    if (work) *work = w;
+    return MOMG_OK;
+  } catch (const Fail& f) {
+    return map_fail(f, err);
+  }
+}
+
 // solve_steady, multigrid.cpp:243-320
 int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_opts* opts,
                       momg_report* report, momg_err* err) {

@@ -617,6 +617,7 @@ struct Launch {
             band_scratch(f, &bp.ver, &bp.next);
             bp.nsweeps = 4 * iters;
             bp.nbands = (f->nx + 15) / 16;
+            bp.nk = bp.nbands;
             bp.dirbits = 0;
             for (int s = 0; s < 16; ++s) bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
             bp.order = ctx.order;
@@ -799,11 +800,35 @@ struct Launch {
     k_norm_partial<M><<<blocks, 256, 0, momg_rt::stream()>>>(res->dev(), field->dev(), partial);
     momg_rt::count_launch(1);
   }
-  // the fused FS iteration + residual over a strip partition (one launch for
-  // this process's strips; first order, M <= 5)
-  static bool strips_sweep_res(const DevCtx& ctx, const StripLaunch& L) {
+  // FS iterations (+ the residual, first order) over a strip partition: one
+  // launch for this process's strips (M <= 5, BGK / Shakhov, no rhs): the
+  // first-order band kernel, or the second-order one with 16-column bands
+  static bool strips_sweep(const DevCtx& ctx, const StripLaunch& L) {
     if constexpr (use_split<M>()) {
-      if (ctx.order != 1 || ctx.collision == 1) return false;
+      if (ctx.collision == 1 || L.iters < 1 || L.iters > 4 || (ctx.order != 1 && L.with_res)) return false;
+      DevCtx c = ctx;
+      if (ctx.order == 2) {
+        sp::Band2Plan bp{};
+        bp.next = L.next;
+        bp.nsweeps = 4 * L.iters;
+        bp.nbands = 2 * L.nbands;
+        for (int s = 0; s < 16; ++s) bp.dirbits |= (unsigned)(L.order[s & 3] & 3) << (2 * s);
+        bp.order = 2;
+        bp.has_rhs = 0;
+        bp.jitter = sched_jitter_seed();
+        bp.strips = (const sp::StripTab*)L.tab;
+        bp.epoch = L.epoch;
+        bp.kb_up = 2 * L.kb_up;
+        bp.kb_dn = 2 * L.kb_dn;
+        bp.nk = 2 * L.nk;
+        bp.sys = L.sys;
+        if constexpr (M == 3) band2_strips_launch_m3(L.geo, c, momg_rt::err_dev(), bp, momg_rt::stream());
+        else if constexpr (M == 4) band2_strips_launch_m4(L.geo, c, momg_rt::err_dev(), bp, momg_rt::stream());
+        else band2_strips_launch_m5(L.geo, c, momg_rt::err_dev(), bp, momg_rt::stream());
+        momg_rt::note_launch(cudaGetLastError());
+        momg_rt::count_launch(1);
+        return true;
+      }
       static bool battr = false;
       if (!battr) {
         set_smem(sp::k5_band<M, 32, false, true>, sp::BandLayout<M>::bytes);
@@ -811,7 +836,7 @@ struct Launch {
       }
       sp::BandPlan bp{};
       bp.next = L.next;
-      bp.nsweeps = 4;
+      bp.nsweeps = 4 * L.iters;
       bp.nbands = L.nbands;
       bp.dirbits = 0;
       for (int s = 0; s < 16; ++s) {
@@ -820,9 +845,14 @@ struct Launch {
       }
       bp.jitter = sched_jitter_seed();
       const int ndiag = std::min(31, L.geo.nx - 1) + L.geo.ny;
-      bp.nchunks = std::max(1, (2 * 148 + L.nk - 1) / L.nk);
-      bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
-      bp.nchunks = (ndiag + bp.clen - 1) / bp.clen;
+      if (L.with_res) {
+        bp.nchunks = std::max(1, (2 * 148 + L.nk - 1) / L.nk);
+        bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
+        bp.nchunks = (ndiag + bp.clen - 1) / bp.clen;
+      } else {
+        bp.nchunks = 0;
+        bp.clen = 1;
+      }
       bp.strips = (const sp::StripTab*)L.tab;
       bp.epoch = L.epoch;
       bp.kb_up = L.kb_up;
@@ -832,7 +862,6 @@ struct Launch {
       int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32, false, true>, sp::BandLayout<M>::bytes, sp::THREADS);
       const int tasks = (bp.nsweeps + bp.nchunks) * bp.nk;
       if (nb > tasks) nb = tasks;
-      DevCtx c = ctx;
       DevField none = L.geo;
       none.c = none.p = nullptr;
       sp::k5_band<M, 32, false, true><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(
@@ -847,7 +876,7 @@ struct Launch {
   }
   static const Ops* ops() {
     static const Ops o = {residual, sweep, restrict_sol, restrict_res, fas, defect, norm_partial, sweep_n, sweep_res,
-                          euler, strips_sweep_res};
+                          euler, strips_sweep};
     return &o;
   }
 };

@@ -54,6 +54,11 @@ __global__ void k_mass_guard(const double* current, DevErr* err) {
   }
 }
 
+__global__ void k_scale_by(double* c, size_t n, double factor) {
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x)
+    c[q] *= factor;
+}
+
 __global__ void k_scale(double* c, size_t n, const double* factor_dev, const DevErr* err) {
   if (err_set(err)) return;
   const double f = *factor_dev;
@@ -1060,6 +1065,19 @@ int momg_defect(const momg_field* res, const momg_field* rhs, momg_field* out, m
   if (!same_shape(res, out) || (rhs && !same_shape(res, rhs)))
     return arg_error(err, "momg_defect: shape mismatch");
   momg_gpu::op_defect(res, rhs, out);
+  return momg_rt::sync_check(err);
+}
+
+// mass_correction's rescale with a factor computed by the caller (a strip of
+// a partitioned level: target / the level's total mass, single_level.cpp:176-183)
+int momg_field_scale(momg_field* f, double factor, momg_err* err) {
+  CLEAR_ERR();
+  ENSURE();
+  ACQ(f);
+  if (!f) return arg_error(err, "momg_field_scale: null field");
+  const size_t n = (size_t)f->nx * f->ny * f->NP;
+  momg_gpu::k_scale_by<<<592, 256, 0, momg_rt::stream()>>>(f->c, n, factor);
+  momg_rt::count_launch(1);
   return momg_rt::sync_check(err);
 }
 

@@ -66,8 +66,10 @@ struct StripLaunch {
   const void* tab;    // device sp::StripTab
   unsigned* next;     // task counter of this process (zeroed by the caller)
   unsigned epoch;     // counters count from here
-  int nbands, kb_up, kb_dn, nk, sys;
+  int nbands, kb_up, kb_dn, nk, sys;  // 32-column bands (the k6 strips variant doubles them)
   int order[4];
+  int iters;     // consecutive FS iterations (<= 4)
+  int with_res;  // append the residual tasks (first order only)
 };
 // Per-moment-order launchers (kernels_m<M>.cu).
 struct Ops {
@@ -81,7 +83,7 @@ struct Ops {
   void (*sweep_n)(const DevCtx&, momg_field*, const momg_field*, const int*, int);
   bool (*sweep_res)(const DevCtx&, momg_field*, const int*, momg_field*, int);
   void (*euler)(const momg_field*, const momg_field*, const momg_field*, const double*);
-  bool (*strips_sweep_res)(const DevCtx&, const StripLaunch&);
+  bool (*strips_sweep)(const DevCtx&, const StripLaunch&);
 };
 const Ops* ops_for(int M);
 DevCtx make_ctx(const momg_ctx* c);

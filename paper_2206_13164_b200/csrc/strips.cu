@@ -20,6 +20,7 @@
 // emulation of all ranks as ONE kernel over all ranks' data (the GPU tests
 // compare it bitwise with the single-field sweep).
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -38,11 +39,19 @@ struct momg_strips {
   std::vector<void*> opened;  // IPC mappings to close
   StripTab tab{};
   StripTab* dtab = nullptr;
-  double* dgeo = nullptr;  // global dx | dy
+  double* dgeo = nullptr;  // global dx | dy | xc | yc
   unsigned* next = nullptr;
   unsigned epoch = 0;
   bool dirty = true;
   bool remote = false;
+  double Ly = 0.0;
+  std::vector<double> hdx, hdy, hxc, hyc;    // global geometry (host)
+  std::vector<momg_field*> ext, ext_res;     // owned strips + halo columns (residual)
+  int strip_of(int i) const {
+    int r = 0;
+    while (r + 1 < n && i >= b[r + 1]) ++r;
+    return r;
+  }
 };
 
 namespace {
@@ -81,6 +90,13 @@ int momg_strips_create(const momg_grid* g, int M, int n, const int* bounds, int 
   s->b.assign(bounds, bounds + n + 1);
   s->field.assign(n, nullptr);
   s->res.assign(n, nullptr);
+  s->ext.assign(n, nullptr);
+  s->ext_res.assign(n, nullptr);
+  s->Ly = g->Ly;
+  s->hdx.assign(g->dx, g->dx + g->nx);
+  s->hdy.assign(g->dy, g->dy + g->ny);
+  s->hxc.assign(g->xc, g->xc + g->nx);
+  s->hyc.assign(g->yc, g->yc + g->ny);
   s->ver.assign(n, nullptr);
   s->present.assign(n, 0);
   s->tab.n = n;
@@ -109,8 +125,10 @@ int momg_strips_create(const momg_grid* g, int M, int n, const int* bounds, int 
     s->present[r] = 1;
   }
   if (rc == MOMG_OK) {
-    std::vector<double> geo(g->dx, g->dx + g->nx);
+    std::vector<double> geo(g->dx, g->dx + g->nx);  // dx | dy | xc | yc
     geo.insert(geo.end(), g->dy, g->dy + g->ny);
+    geo.insert(geo.end(), g->xc, g->xc + g->nx);
+    geo.insert(geo.end(), g->yc, g->yc + g->ny);
     if (cudaMalloc(&s->dgeo, geo.size() * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&s->dtab, sizeof(StripTab)) != cudaSuccess || cudaMalloc(&s->next, 64) != cudaSuccess)
       rc = fail(err, MOMG_ERR_CUDA, "momg_strips_create: allocation failed");
@@ -133,6 +151,8 @@ void momg_strips_destroy(momg_strips* s) {
   for (int r = 0; r < s->n; ++r) {
     momg_gpu::field_free(s->field[r]);
     momg_gpu::field_free(s->res[r]);
+    momg_gpu::field_free(s->ext[r]);
+    momg_gpu::field_free(s->ext_res[r]);
     cudaFree(s->ver[r]);
   }
   cudaFree(s->dtab);
@@ -184,17 +204,20 @@ int momg_strips_import(momg_strips* s, int r, const void* handle, momg_err* err)
   return MOMG_OK;
 }
 
-int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const int* sweep_order, long long* evals,
-                                    momg_err* err) {
+// one band launch over this process's strips: `iters` FS iterations, plus
+// the residual tasks when with_res (first order)
+static int strips_launch(const momg_ctx* ctx, momg_strips* s, const int* sweep_order, int iters, int with_res,
+                         long long* evals, momg_err* err, const char* who) {
   if (err) err->code = 0;
   if (int rc = momg_rt::ensure(err)) return rc;
-  if (!ctx || !s) return fail(err, MOMG_ERR_ARG, "momg_strips_fast_sweep_residual: null argument");
-  if (ctx->M != s->M) return fail(err, MOMG_ERR_ARG, "momg_strips_fast_sweep_residual: moment order mismatch");
+  if (!ctx || !s) return fail(err, MOMG_ERR_ARG, "momg_strips: null argument");
+  if (ctx->M != s->M) return fail(err, MOMG_ERR_ARG, "momg_strips: moment order mismatch");
   if (!(ctx->knudsen > 0)) return fail(err, MOMG_CONFIG, "collision_frequency: Kn must be positive");
+  if (iters < 1 || iters > 4) return fail(err, MOMG_ERR_ARG, "momg_strips: 1 <= iterations per launch <= 4");
   // every strip a task may touch must be attached: the neighbours of the owned range
   const int lo = s->first > 0 ? s->first - 1 : 0, hi = s->last + 1 < s->n ? s->last + 1 : s->n - 1;
   for (int r = lo; r <= hi; ++r)
-    if (!s->present[r]) return fail(err, MOMG_ERR_ARG, "momg_strips_fast_sweep_residual: neighbour strip not attached");
+    if (!s->present[r]) return fail(err, MOMG_ERR_ARG, "momg_strips: neighbour strip not attached");
   for (int r = s->first; r <= s->last; ++r) momg_rt::acquire(s->field[r]);
   if (s->dirty) {
     cudaMemcpyAsync(s->dtab, &s->tab, sizeof(StripTab), cudaMemcpyHostToDevice, momg_rt::stream());
@@ -206,6 +229,8 @@ int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const i
   L.geo.ny = s->ny;
   L.geo.dx = s->dgeo;
   L.geo.dy = s->dgeo + s->nx;
+  L.geo.xc = s->dgeo + s->nx + s->ny;
+  L.geo.yc = s->dgeo + 2 * s->nx + s->ny;
   L.tab = s->dtab;
   L.next = s->next;
   L.epoch = s->epoch;
@@ -214,14 +239,119 @@ int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const i
   L.kb_dn = (s->nx - s->b[s->last + 1]) / 32;
   L.nk = (s->b[s->last + 1] - s->b[s->first]) / 32;
   L.sys = s->remote ? 1 : 0;
+  L.iters = iters;
+  L.with_res = with_res;
   static const int canon[4] = {0, 1, 2, 3};
   for (int k = 0; k < 4; ++k) L.order[k] = (sweep_order ? sweep_order : canon)[k];
-  s->epoch += 4;  // every rank advances identically, launched or not
-  if (!momg_gpu::ops_for(s->M)->strips_sweep_res(momg_gpu::make_ctx(ctx), L))
-    return fail(err, MOMG_CONFIG, "momg_strips_fast_sweep_residual: strips run first order, M <= 5, BGK / Shakhov");
+  s->epoch += 4u * (unsigned)iters;  // every rank advances identically, launched or not
+  if (!momg_gpu::ops_for(s->M)->strips_sweep(momg_gpu::make_ctx(ctx), L))
+    return fail(err, MOMG_CONFIG, who);
   const int rc = momg_rt::sync_check(err);
-  if (rc == MOMG_OK && evals) *evals += 4LL * (s->b[s->last + 1] - s->b[s->first]) * s->ny;
+  if (rc == MOMG_OK && evals) *evals += 4LL * iters * (s->b[s->last + 1] - s->b[s->first]) * s->ny;
   return rc;
+}
+
+// columns [i0, i1) of the level, from whichever strips hold them (own or
+// peer memory), into dst at column x0 (dst: a field of width dnx); which =
+// 0: the strips' fields, 1: their residual fields
+static void copy_cols(const momg_strips* s, int which, int i0, int i1, momg_field* dst, int x0) {
+  const int NP = dst->NP;
+  for (int r = 0; r < s->n; ++r) {
+    const int a = std::max(i0, s->b[r]), e = std::min(i1, s->b[r + 1]);
+    if (a >= e) continue;
+    const int w = s->b[r + 1] - s->b[r];
+    const double* sc = which ? s->tab.oc[r] : s->tab.c[r];
+    const double* sp = which ? s->tab.op[r] : s->tab.p[r];
+    const int dx0 = x0 + (a - i0);
+    cudaMemcpy2DAsync(dst->c + (size_t)dx0 * NP, (size_t)dst->nx * NP * sizeof(double), sc + (size_t)(a - s->b[r]) * NP,
+                      (size_t)w * NP * sizeof(double), (size_t)(e - a) * NP * sizeof(double), s->ny, cudaMemcpyDefault,
+                      momg_rt::stream());
+    cudaMemcpy2DAsync(dst->p + (size_t)dx0 * 4, (size_t)dst->nx * 4 * sizeof(double), sp + (size_t)(a - s->b[r]) * 4,
+                      (size_t)w * 4 * sizeof(double), (size_t)(e - a) * 4 * sizeof(double), s->ny, cudaMemcpyDefault,
+                      momg_rt::stream());
+  }
+}
+
+int momg_strips_fast_sweep_residual(const momg_ctx* ctx, momg_strips* s, const int* sweep_order, long long* evals,
+                                    momg_err* err) {
+  return strips_launch(ctx, s, sweep_order, 1, 1, evals, err,
+                       "momg_strips_fast_sweep_residual: strips run first order, M <= 5, BGK / Shakhov");
+}
+
+int momg_strips_fast_sweep(const momg_ctx* ctx, momg_strips* s, const int* sweep_order, int iters, long long* evals,
+                           momg_err* err) {
+  return strips_launch(ctx, s, sweep_order, iters, 0, evals, err,
+                       "momg_strips_fast_sweep: strips run M <= 5, BGK / Shakhov");
+}
+
+int momg_strips_residual(const momg_ctx* ctx, momg_strips* s, momg_err* err) {
+  if (err) err->code = 0;
+  if (int rc = momg_rt::ensure(err)) return rc;
+  if (!ctx || !s || ctx->M != s->M) return fail(err, MOMG_ERR_ARG, "momg_strips_residual: bad arguments");
+  const int h = ctx->space_order == 2 ? 2 : 1;  // stencil radius (spatial.cpp:34-50, 98-124)
+  const momg_gpu::DevCtx dctx = momg_gpu::make_ctx(ctx);
+  for (int r = s->first; r <= s->last; ++r) {
+    const int lo = std::max(0, s->b[r] - h), hi = std::min(s->nx, s->b[r + 1] + h);
+    for (int q = lo; q < hi; ++q)
+      if (!s->present[s->strip_of(q)]) return fail(err, MOMG_ERR_ARG, "momg_strips_residual: neighbour strip not attached");
+    momg_rt::acquire(s->field[r]);
+    if (!s->ext[r]) {
+      // the strip plus its neighbours' h columns: the residual of the strip's
+      // own cells on this field is the level's (their stencils lie inside it)
+      const int w = hi - lo;
+      std::vector<double> dx(s->hdx.begin() + lo, s->hdx.begin() + hi), xc(s->hxc.begin() + lo, s->hxc.begin() + hi);
+      double Lx = 0.0;
+      for (double v : dx) Lx += v;
+      for (momg_field** f : {&s->ext[r], &s->ext_res[r]}) {
+        *f = momg_gpu::field_new(s->M, w, s->ny, Lx, s->Ly, dx.data(), s->hdy.data(), xc.data(), s->hyc.data(), err);
+        if (!*f) return err ? err->code : MOMG_ERR_CUDA;
+      }
+    }
+    copy_cols(s, 0, lo, hi, s->ext[r], 0);
+    momg_gpu::op_residual(dctx, s->ext[r], s->ext_res[r]);
+    // the strip's own columns of the residual
+    const int NP = s->ext_res[r]->NP, w = s->b[r + 1] - s->b[r], off = s->b[r] - lo, W = hi - lo;
+    cudaMemcpy2DAsync(s->res[r]->c, (size_t)w * NP * sizeof(double), s->ext_res[r]->c + (size_t)off * NP,
+                      (size_t)W * NP * sizeof(double), (size_t)w * NP * sizeof(double), s->ny, cudaMemcpyDeviceToDevice,
+                      momg_rt::stream());
+    cudaMemcpy2DAsync(s->res[r]->p, (size_t)w * 4 * sizeof(double), s->ext_res[r]->p + (size_t)off * 4,
+                      (size_t)W * 4 * sizeof(double), (size_t)w * 4 * sizeof(double), s->ny, cudaMemcpyDeviceToDevice,
+                      momg_rt::stream());
+  }
+  return momg_rt::sync_check(err);
+}
+
+int momg_strips_gather(momg_strips* s, int which, momg_field* full, momg_err* err) {
+  if (err) err->code = 0;
+  if (int rc = momg_rt::ensure(err)) return rc;
+  if (!s || !full || full->nx != s->nx || full->ny != s->ny || full->M != s->M)
+    return fail(err, MOMG_ERR_ARG, "momg_strips_gather: the full field must have the level's shape");
+  for (int r = 0; r < s->n; ++r)
+    if (!s->present[r]) return fail(err, MOMG_ERR_ARG, "momg_strips_gather: strip not attached");
+  for (int r = s->first; r <= s->last; ++r) momg_rt::acquire(which ? s->res[r] : s->field[r]);
+  momg_rt::acquire(full);
+  copy_cols(s, which, 0, s->nx, full, 0);
+  return momg_rt::sync_check(err);
+}
+
+int momg_strips_scatter(momg_strips* s, int which, const momg_field* full, momg_err* err) {
+  if (err) err->code = 0;
+  if (int rc = momg_rt::ensure(err)) return rc;
+  if (!s || !full || full->nx != s->nx || full->ny != s->ny || full->M != s->M)
+    return fail(err, MOMG_ERR_ARG, "momg_strips_scatter: the full field must have the level's shape");
+  momg_rt::acquire(full);
+  for (int r = s->first; r <= s->last; ++r) {
+    momg_field* dst = which ? s->res[r] : s->field[r];
+    momg_rt::acquire(dst);
+    const int NP = dst->NP, w = s->b[r + 1] - s->b[r];
+    cudaMemcpy2DAsync(dst->c, (size_t)w * NP * sizeof(double), full->c + (size_t)s->b[r] * NP,
+                      (size_t)s->nx * NP * sizeof(double), (size_t)w * NP * sizeof(double), s->ny,
+                      cudaMemcpyDeviceToDevice, momg_rt::stream());
+    cudaMemcpy2DAsync(dst->p, (size_t)w * 4 * sizeof(double), full->p + (size_t)s->b[r] * 4,
+                      (size_t)s->nx * 4 * sizeof(double), (size_t)w * 4 * sizeof(double), s->ny,
+                      cudaMemcpyDeviceToDevice, momg_rt::stream());
+  }
+  return momg_rt::sync_check(err);
 }
 
 }  // extern "C"

@@ -598,6 +598,32 @@ class StripSet:
             p[:, i0:i1] = sp.reshape(self.grid.ny, i1 - i0, 4)
         return c.reshape(-1, n), p.reshape(-1, 4)
 
+    def fast_sweep(self, ctx: SolveContext, iters: int = 1, sweep_order=(0, 1, 2, 3),
+                   work: WorkStats | None = None):
+        """`iters` (<= 4) consecutive fast_sweep_step calls over the partition, one launch."""
+        err = _Err()
+        c = ctx._c(self.order)
+        ev = C.c_longlong(0)
+        order = (C.c_int * 4)(*sweep_order)
+        rc = lib().momg_strips_fast_sweep(C.byref(c), self._h, order, iters, C.byref(ev), C.byref(err))
+        if work is not None:
+            work.cell_evals += ev.value
+        _raise(rc, err)
+
+    def residual(self, ctx: SolveContext):
+        """residual of the owned strips into their residual fields."""
+        err = _Err()
+        c = ctx._c(self.order)
+        _raise(lib().momg_strips_residual(C.byref(c), self._h, C.byref(err)), err)
+
+    def gather(self, which: int, full: CellField):
+        err = _Err()
+        _raise(lib().momg_strips_gather(self._h, which, full._h, C.byref(err)), err)
+
+    def scatter(self, which: int, full: CellField):
+        err = _Err()
+        _raise(lib().momg_strips_scatter(self._h, which, full._h, C.byref(err)), err)
+
     def fast_sweep_residual(self, ctx: SolveContext, sweep_order=(0, 1, 2, 3), work: WorkStats | None = None):
         err = _Err()
         c = ctx._c(self.order)
@@ -607,6 +633,27 @@ class StripSet:
         if work is not None:
             work.cell_evals += ev.value
         _raise(rc, err)
+
+
+def field_scale(field: CellField, factor: float) -> None:
+    """coeffs *= factor (mass_correction's rescale with a caller-computed factor)."""
+    err = _Err()
+    _raise(lib().momg_field_scale(field._h, C.c_double(factor), C.byref(err)), err)
+
+
+def nmg_cycle_rhs(field: CellField, rhs: CellField | None, ctx: SolveContext, levels: int = 0,
+                  policy: CyclePolicy | None = None, work: WorkStats | None = None) -> None:
+    """nmg_cycle for R(f) = rhs on GridHierarchy::build(field grid, levels)
+    (multigrid.cpp:166-200), the coarse problem of an outer cycle."""
+    p = policy or CyclePolicy()
+    err = _Err()
+    c = ctx._c(field.order)
+    w = C.c_longlong(0)
+    rc = lib().momg_nmg_cycle_rhs(C.byref(c), field._h, rhs._h if rhs is not None else None, levels, p.s1, p.s2,
+                                  p.s3, p.gamma, C.byref(w), C.byref(err))
+    if work is not None:
+        work.cell_evals += w.value
+    _raise(rc, err)
 
 
 def synchronize() -> None:

@@ -105,10 +105,11 @@ class StripLevel:
     """One level of a rank-partitioned field: this rank's strip on its GPU
     (all strips when world == 1), neighbours attached over IPC."""
 
-    def __init__(self, momg, grid, order: int, comm: StripComm, emulate_ranks: int | None = None):
+    def __init__(self, momg, grid, order: int, comm: StripComm, emulate_ranks: int | None = None,
+                 bounds: Sequence[int] | None = None, band: int = BAND):
         self.momg, self.grid, self.order, self.comm = momg, grid, order, comm
         nr = emulate_ranks if comm.world == 1 else comm.world
-        self.bounds = strip_bounds(grid.nx, nr if nr else 1)
+        self.bounds = list(bounds) if bounds is not None else strip_bounds(grid.nx, nr if nr else 1, band)
         if comm.world == 1:
             self.owned = list(range(len(self.bounds) - 1))
             self.set = momg.StripSet(grid, order, self.bounds)
@@ -117,8 +118,9 @@ class StripLevel:
             self.owned = [r]
             self.set = momg.StripSet(grid, order, self.bounds, first=r, last=r)
             handles = comm.allgather_bytes(self.set.export(r))
-            for peer in (r - 1, r + 1):
-                if 0 <= peer < comm.world:
+            # every peer strip (the sweep needs the neighbours, a gather all)
+            for peer in range(comm.world):
+                if peer != r:
                     self.set.attach(peer, handles[peer])
 
     def field(self, r):
@@ -147,3 +149,119 @@ class StripLevel:
         loc = [(self.momg.residual_norm(self.residual_field(r), self.field(r)), self.field(r).grid.Lx)
                for r in self.owned]
         return combine_norm(self.comm, loc, self.grid.Lx, self.grid.Ly)
+
+
+def coarse_grid(momg, g):
+    """coarsen (multigrid.cpp:12-35): 2x2 agglomeration of a Grid2D."""
+    import numpy as np
+    dx = np.asarray(g.dx[0::2]) + np.asarray(g.dx[1::2])
+    dy = np.asarray(g.dy[0::2]) + np.asarray(g.dy[1::2])
+    return momg.Grid2D(g.nx // 2, g.ny // 2, g.Lx, g.Ly, dx, dy, np.cumsum(dx) - 0.5 * dx, np.cumsum(dy) - 0.5 * dy)
+
+
+class StripSolver:
+    """solve_steady (multigrid.cpp:243-320) with the NMG V-cycle (:166-200)
+    whose FINEST level is strip-partitioned across the ranks and whose
+    coarser levels are agglomerated on every rank: each rank restricts its
+    strip, the coarse strips are gathered (peer memory) into a full coarse
+    level on every rank, every rank runs the identical coarse cycle
+    (momg_nmg_cycle_rhs, deterministic), and each rank prolongs (FAS) into
+    its own strip.  The finest level holds ~3/4 of the work; the coarse
+    levels are small.  Strip widths are multiples of 64 so the coarse strips
+    are whole 32-column bands too.  The operation sequence is the single-field
+    driver's (driver.cu), so the result equals a one-GPU solve up to the
+    summation order of the combined mass and norm."""
+
+    def __init__(self, momg, grid, order: int, comm: StripComm, levels: int, policy=None,
+                 emulate_ranks: int | None = None):
+        self.momg, self.comm, self.levels = momg, comm, levels
+        self.policy = policy or momg.CyclePolicy()
+        self.fine = StripLevel(momg, grid, order, comm, emulate_ranks, band=2 * BAND)
+        cg = coarse_grid(momg, grid)
+        self.coarse = StripLevel(momg, cg, order, comm, bounds=[b // 2 for b in self.fine.bounds])
+        self.cgrid = cg
+        self.Fc, self.Fb = momg.CellField(cg, order), momg.CellField(cg, order)
+        self.crhs, self.cres = momg.CellField(cg, order), momg.CellField(cg, order)
+        self.work = momg.WorkStats()
+
+    def _fence(self):
+        self.comm.fence(self.momg.synchronize)
+
+    def _sweeps(self, ctx, n):
+        while n > 0:
+            k = min(n, 4)
+            self._fence()
+            self.fine.set.fast_sweep(ctx, k, work=self.work)
+            n -= k
+        self._fence()
+
+    def _call(self, name, *args):
+        m = self.momg
+        err = m._Err()
+        m._raise(getattr(m.lib(), name)(*[a.handle if hasattr(a, "handle") else a for a in args], m.C.byref(err)), err)
+
+    def cycle(self, ctx):
+        m, f, c, pol = self.momg, self.fine, self.coarse, self.policy
+        self._sweeps(ctx, pol.s1)
+        f.set.residual(ctx)
+        for r in f.owned:
+            fr, rr = f.field(r), f.residual_field(r)
+            self._call("momg_defect", rr, None, rr)
+            self._call("momg_restrict_solution", fr, c.field(r))
+            self._call("momg_restrict_residual", rr, c.field(r), c.residual_field(r))
+        self._fence()
+        c.set.gather(0, self.Fc)
+        c.set.gather(1, self.crhs)
+        self._call("momg_field_copy", self.Fb, self.Fc)
+        self._res(ctx)
+        self._call("momg_axpy", self.crhs, self.cres)
+        for _ in range(pol.gamma):
+            m.nmg_cycle_rhs(self.Fc, self.crhs, ctx, self.levels - 1, pol, self.work)
+        c.set.scatter(0, self.Fc)
+        c.set.scatter(1, self.Fb)
+        for r in f.owned:
+            self._call("momg_fas_correct", f.field(r), c.residual_field(r), c.field(r))
+        self._sweeps(ctx, pol.s2)
+
+    def _res(self, ctx):
+        m = self.momg
+        err = m._Err()
+        cc = ctx._c(self.Fc.order)
+        m._raise(m.lib().momg_residual(m.C.byref(cc), self.Fc.handle, self.cres.handle, m.C.byref(err)), err)
+        return self.cres
+
+    def norm(self, ctx):
+        self.fine.set.residual(ctx)
+        return self.fine.residual_norm()
+
+    def solve(self, ctx, tol: float = 1e-8, max_iterations: int = 0):
+        """The loop of solve_steady; returns (converged, iterations, history)."""
+        m = self.momg
+        cap = max_iterations or 200
+        self._fence()
+        r0 = self.norm(ctx)
+        scale = self.comm.allreduce_max(max(m.residual_scale(self.fine.field(r), ctx) for r in self.fine.owned))
+        if r0 <= 1e-12 * scale:
+            return True, 0, []
+        target = self.fine.total_mass()
+        hist = []
+        for n in range(1, cap + 1):
+            try:
+                self.cycle(ctx)
+                current = self.fine.total_mass()
+                if not (current > 0.0) or not math.isfinite(current):
+                    raise m.NonphysicalState(f"mass_correction: nonpositive total mass {current}")
+                for r in self.fine.owned:
+                    m.field_scale(self.fine.field(r), target / current)
+                self._fence()
+                ratio = self.norm(ctx) / r0
+            except (m.SolverError, m.NonphysicalState) as e:
+                raise m.NonConvergence(f"iteration step failed: {e}",
+                                       m.SolveReport(False, n - 1, r0, 0.0, 0.0, self.work.cell_evals, 0.0, hist))
+            hist.append(ratio)
+            if not math.isfinite(ratio) or ratio > 1e6:
+                raise m.NonConvergence(f"residual diverged: ratio {ratio} at iteration {n}",
+                                       m.SolveReport(False, n, r0, 0.0, ratio, self.work.cell_evals, 0.0, hist))
+            if ratio <= tol:
+                return True, n, hist
+        return False, cap, hist
