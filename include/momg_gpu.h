@@ -69,7 +69,7 @@ typedef struct momg_ctx {
   double viscosity_index; /* GasParams.viscosity_index */
   double wall_speed[4];
   double wall_theta[4];
-  int threads;         /* accepted for API parity; ignored (device-parallel) */
+  int threads;         /* SolveContext.threads: > 1 selects the blocked-parallel sweep (band-aligned blocks, first order) */
 } momg_ctx;
 
 /* CyclePolicy + SolverOptions (multigrid.hpp:30-35, 101-107). */

@@ -88,6 +88,16 @@ struct BandPlan {
   unsigned epoch;
   int kb_up, kb_dn, nk;
   int sys;
+  // blocked mode (SolveContext.threads = T > 1 on band-aligned blocks; the
+  // reference's threads > 1 sweep, single_level.cpp:130-161, realised
+  // deterministically): korder[f * nbands + pos] = the band claimed at
+  // position pos of a sweep in frame f (0: i ascending, 1: descending) --
+  // blocks in descending rotated order, bands ascending inside a block;
+  // bflags[f * nbands + k]: 1 = the band starts a block (its x-upstream halo
+  // is the OLD state, that block runs later), 2 = it ends one (the next
+  // band's first column is the NEW state, that block ran earlier)
+  const short* korder;
+  const unsigned char* bflags;
 };
 
 template <int M>
@@ -171,26 +181,29 @@ __device__ __forceinline__ bool band_stop(const DevErr* err) {
 template <int M, int MAXS, class Addr, class Geo>
 __device__ __forceinline__ void band_load(const Addr& fld, const Geo& b, int dd, int s0, int ns,
                                           unsigned need, double* vec, int vstride, double* prm, int wi, int nw,
-                                          DevErr* err, int poll_ns, unsigned jit = 0, bool sys = false) {
+                                          DevErr* err, int poll_ns, unsigned jit = 0, bool sys = false,
+                                          int hi_slot = 1 << 30, unsigned hi_need = 0) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, H = (N + 31) / 32;
   static_assert(MAXS <= 32, "one polling lane per slot");
   constexpr int PR = (4 * MAXS + 31) / 32;  // rounds of parameter loads (4 lanes per slot)
   const int lane = threadIdx.x & 31;
   int my_cell = -1;
+  unsigned my_need = need;
   if (lane < MAXS) {
     const int slot = s0 + wi + lane * nw;
     if (slot < s0 + ns) my_cell = b.cell(slot, dd);
+    if (slot == hi_slot) my_need = hi_need;
   }
   if (jit && need) sched_jitter(jit, (unsigned)dd);
-  if (need && my_cell >= 0) {
+  if (my_need && my_cell >= 0) {
     // relaxed polling, one acquire once satisfied (an acquire per poll
     // measured slower: the spinning warps slow the SM's memory pipeline)
     const unsigned* a = fld.vptr(my_cell);
     long long polls = 0;
-    while (ld_relaxed_s(a, Addr::kStrips && sys) < need) {
+    while (ld_relaxed_s(a, Addr::kStrips && sys) < my_need) {
       if (band_stop(err)) break;
       if (++polls > (1LL << 26)) {
-        tc::raise(err, E_ERROR, W_DEADLOCK, my_cell % b.nx, my_cell / b.nx, (double)need);
+        tc::raise(err, E_ERROR, W_DEADLOCK, my_cell % b.nx, my_cell / b.nx, (double)my_need);
         break;
       }
       if (poll_ns) __nanosleep(poll_ns);
@@ -341,7 +354,12 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     const int s = res ? plan.nsweeps - 1 : task / plan.nk;
     // residual tasks walk the frame of the last sweep, whose wavefront they follow
     const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
-    const int k = (dir == 0 || dir == 3 ? plan.kb_up : plan.kb_dn) + (res ? rtask : task) % plan.nk;
+    const int frame = dir == 0 || dir == 3 ? 0 : 1;
+    const int pos = (res ? rtask : task) % plan.nk;
+    const int k = (!res && plan.korder) ? (int)plan.korder[frame * plan.nbands + pos]
+                                        : (frame == 0 ? plan.kb_up : plan.kb_dn) + pos;
+    const int bfl = (!res && plan.bflags) ? (int)plan.bflags[frame * plan.nbands + k] : 0;
+    const bool bstart = (bfl & 1) != 0, bend = (bfl & 2) != 0;  // blocked mode (see BandPlan)
     BandGeo<ST> b;
     b.nx = f.nx;
     b.ny = f.ny;
@@ -373,7 +391,9 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
     if (!res && warp == 0) {
       for (int e = c; e < 2 * NS + 1; e += 32) {
         const int cl = e < 2 * NS ? b.cell(e % NS, dfirst + e / NS) : (k > 0 ? b.cell(-1, dfirst - 1) : -1);
-        const unsigned need = ep + (e < 2 * NS ? (unsigned)s : (unsigned)s + 1u);
+        // halo: new (old at a block start); row dfirst+1's slot NS-1: old (new at a block end)
+        const unsigned need = ep + (e < 2 * NS ? (unsigned)s + (bend && e == 2 * NS - 1 ? 1u : 0u)
+                                                : (unsigned)s + (bstart ? 0u : 1u));
         if (cl >= 0 && need) {
           long long polls = 0;
           const unsigned* a = fa.vptr(cl);
@@ -626,13 +646,14 @@ __global__ void __launch_bounds__(THREADS, 1) k5_band(DevField f, DevCtx ctx, De
 
         if (d + 1 <= dlast)
           band_load<M, 5>(fa, b, d + 2, 0, NS, res ? rneed : ep + (unsigned)s, smem + LY::V_X * VEC, SPV,
-                          smem + LY::PX, wi, npw, err, plan.poll_ns, plan.jitter, sys);
+                          smem + LY::PX, wi, npw, err, plan.poll_ns, plan.jitter, sys,
+                          bend ? NS - 1 : 1 << 30, ep + (unsigned)s + 1u);
         if (res && wi == 0 && d + 1 <= dlast)  // (the sweep: group 1 does this)
           band_pre<M, BW>(f, ctx, b, d + 1, smem + LY::V_OLD1 * VEC, smem + LY::PO,
                           smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         // band k-1's new cell last: by then it is (nearly always) published
         if (k > 0 && wi == npw - 1 && d + 1 <= dlast)
-          band_load<M, 1>(fa, b, d, -1, 1, res ? rneed : ep + (unsigned)s + 1u, smem + LY::HALO, 1,
+          band_load<M, 1>(fa, b, d, -1, 1, res ? rneed : ep + (unsigned)s + (bstart ? 0u : 1u), smem + LY::HALO, 1,
                           smem + LY::HALOP, 0, 1, err, plan.poll_ns, plan.jitter, sys);
         if (wi == 0 && c == 0) {
           s_stop = stop_now;

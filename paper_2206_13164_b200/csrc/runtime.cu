@@ -363,6 +363,7 @@ DevCtx make_ctx(const momg_ctx* c) {
   d.nu_exp = 1.0 - c->viscosity_index;
   d.shakhov_w = (1.0 - c->prandtl) / 5.0;
   d.prandtl = c->prandtl;
+  d.threads = c->threads;
   for (int w = 0; w < 4; ++w) {
     d.wall_speed[w] = c->wall_speed[w];
     d.wall_theta[w] = c->wall_theta[w];
@@ -470,6 +471,58 @@ long long read_trace(unsigned long long* host, long long n) {
 unsigned sched_jitter_seed() {
   const char* e = std::getenv("MOMG_JITTER");
   return e ? (unsigned)std::strtoul(e, nullptr, 10) : 0u;
+}
+
+// Blocked-parallel sweep plan (BandPlan::korder / bflags) for T workers on
+// nbands 32-column bands: the reference's blocks [nx b / T, nx (b+1) / T)
+// (single_level.cpp:137-141) when every boundary is a band boundary, else
+// null (the exact order, itself one outcome of the reference's blocked run:
+// the workers finishing in block order).  Cached per (T, nx).
+bool blocked_plan(int T, int nx, const short** korder, const unsigned char** bflags) {
+  *korder = nullptr;
+  *bflags = nullptr;
+  if (T <= 1 || nx % 32 || T > nx) return false;
+  const int nb = nx / 32;
+  std::vector<int> lo(T + 1);
+  for (int b = 0; b <= T; ++b) {
+    lo[b] = (int)((long long)nx * b / T);
+    if (lo[b] % 32) return false;
+  }
+  struct Entry {
+    int T, nx;
+    short* ko;
+    unsigned char* bf;
+  };
+  static std::vector<Entry> cache;
+  for (const Entry& e : cache)
+    if (e.T == T && e.nx == nx) {
+      *korder = e.ko;
+      *bflags = e.bf;
+      return true;
+    }
+  std::vector<short> ko(2 * nb);
+  std::vector<unsigned char> bf(2 * nb, 0);
+  for (int fr = 0; fr < 2; ++fr) {
+    std::vector<int> rb;  // rotated block boundaries in bands, ascending
+    for (int b = 0; b <= T; ++b) rb.push_back(fr == 0 ? lo[b] / 32 : (nx - lo[T - b]) / 32);
+    int pos = 0;
+    for (int t = T - 1; t >= 0; --t) {  // blocks in descending rotated order
+      for (int k = rb[t]; k < rb[t + 1]; ++k) ko[fr * nb + pos++] = (short)k;
+      if (rb[t + 1] > rb[t]) {
+        if (t > 0) bf[fr * nb + rb[t]] |= 1;
+        if (t + 1 < T) bf[fr * nb + rb[t + 1] - 1] |= 2;
+      }
+    }
+  }
+  Entry e{T, nx, nullptr, nullptr};
+  cudaMalloc(&e.ko, ko.size() * sizeof(short));
+  cudaMalloc(&e.bf, bf.size());
+  cudaMemcpy(e.ko, ko.data(), ko.size() * sizeof(short), cudaMemcpyHostToDevice);
+  cudaMemcpy(e.bf, bf.data(), bf.size(), cudaMemcpyHostToDevice);
+  cache.push_back(e);
+  *korder = e.ko;
+  *bflags = e.bf;
+  return true;
 }
 
 void band_scratch(momg_field* f, unsigned** ver, unsigned** next) {

@@ -62,6 +62,7 @@ struct DevCtx {
   double nu_exp;       // 1 - viscosity_index
   double shakhov_w;    // (1 - Pr)/5 (collision.hpp:99)
   double prandtl;
+  int threads;         // SolveContext.threads (blocked-parallel sweeps when > 1)
   double wall_speed[4];  // left, right, bottom, top
   double wall_theta[4];
 };
