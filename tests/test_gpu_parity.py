@@ -362,7 +362,7 @@ def test_c1_against_reference_golden():
 def test_c2_against_reference_golden():
     """BASELINE configs[1] (C2): 128^2, M=5, second order, BGK Kn 0.1, NMG over
     4 levels (V(2,2), s3=4) to 1e-8.  Golden = the CPU oracle run (99 NMG
-    iterations, 1065 s single-threaded), pinned bitwise to the reference."""
+    iterations, 1231 s single-threaded): the reference itself (oracle/_ref, tools/make_golden.py)."""
     z = _golden("c2.npz")
     M = 5
     g = Grid.uniform(128, 128)

@@ -99,8 +99,11 @@ def c1(R):
 
 
 def c2():
-    js = os.path.join(OUT, "configs_C2_port.json")
-    fz = os.path.join(OUT, "configs_C2_port_field.npz")
+    # the reference's own run when present (python tools/run_oracle_configs.py C2 --ref,
+    # 99 iterations, ~20 min on one core), else the bitwise-pinned port's
+    kind = "reference" if os.path.exists(os.path.join(OUT, "configs_C2_reference.json")) else "port"
+    js = os.path.join(OUT, f"configs_C2_{kind}.json")
+    fz = os.path.join(OUT, f"configs_C2_{kind}_field.npz")
     if not (os.path.exists(js) and os.path.exists(fz)):
         print("C2 oracle run missing: python tools/run_oracle_configs.py C2")
         return
@@ -111,7 +114,7 @@ def c2():
     macro = np.concatenate([c[:, :1], p, q, 2 * c[:, 4:5], c[:, 5:6], 2 * c[:, 7:8]], axis=1)
     np.savez_compressed(os.path.join(OUT, "c2.npz"), macro=macro, history=np.array(rep["history"]),
                         iterations=rep["iterations"], c_bound=rep["config"]["c_bound"],
-                        oracle_seconds=rep["wall_s"])
+                        oracle_seconds=rep["wall_s"], kind=kind)
 
 
 if __name__ == "__main__":
