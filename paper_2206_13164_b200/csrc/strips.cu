@@ -47,6 +47,7 @@ struct momg_strips {
   double Ly = 0.0;
   std::vector<double> hdx, hdy, hxc, hyc;    // global geometry (host)
   std::vector<momg_field*> ext, ext_res;     // owned strips + halo columns (residual)
+  std::vector<int> ext_h;                    // their halo width (1 or 2: the stencil radius)
   int strip_of(int i) const {
     int r = 0;
     while (r + 1 < n && i >= b[r + 1]) ++r;
@@ -92,6 +93,7 @@ int momg_strips_create(const momg_grid* g, int M, int n, const int* bounds, int 
   s->res.assign(n, nullptr);
   s->ext.assign(n, nullptr);
   s->ext_res.assign(n, nullptr);
+  s->ext_h.assign(n, 0);
   s->Ly = g->Ly;
   s->hdx.assign(g->dx, g->dx + g->nx);
   s->hdy.assign(g->dy, g->dy + g->ny);
@@ -295,7 +297,13 @@ int momg_strips_residual(const momg_ctx* ctx, momg_strips* s, momg_err* err) {
     for (int q = lo; q < hi; ++q)
       if (!s->present[s->strip_of(q)]) return fail(err, MOMG_ERR_ARG, "momg_strips_residual: neighbour strip not attached");
     momg_rt::acquire(s->field[r]);
+    if (s->ext[r] && s->ext_h[r] != h) {  // the other spatial order: other halo width
+      momg_gpu::field_free(s->ext[r]);
+      momg_gpu::field_free(s->ext_res[r]);
+      s->ext[r] = s->ext_res[r] = nullptr;
+    }
     if (!s->ext[r]) {
+      s->ext_h[r] = h;
       // the strip plus its neighbours' h columns: the residual of the strip's
       // own cells on this field is the level's (their stencils lie inside it)
       const int w = hi - lo;
