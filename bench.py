@@ -507,6 +507,22 @@ def run_nmg_c2(momg):
                         "note": "FS flops only (residual / transfer work excluded); the V-cycle is bound by "
                                 "the DAG depth of the exact-order sweeps x the per-diagonal step latency"}}
     out["cpu"] = nmg_cpu_c2(rep.iterations)
+    # the reference's threads > 1 semantics on the device (blocked-parallel
+    # sweeps, 8 workers: one 16-column band per block on the 128^2 level;
+    # coarser levels' blocks are not band-aligned and run the exact order)
+    ctx8 = momg.cavity_context(5, 2, knudsen=0.1, lid=0.1)
+    ctx8.threads = 8
+    f8 = momg.uniform_field(g, 5, 1.0, (0.0, 0.0, 0.0), 1.0)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    try:
+        rep8 = momg.solve_steady(f8, ctx8, momg.SolverOptions(momg.SolverKind.nmg, 1e-8, 0, 4))
+        ok8 = True
+    except momg.NonConvergence as e:
+        rep8, ok8 = e.report, False
+    out["blocked_threads8"] = {"seconds": time.perf_counter() - t, "converged": ok8, "iterations": rep8.iterations,
+                               "note": "SolveContext.threads = 8 (the reference's blocked-parallel FS realised "
+                                       "deterministically, DESIGN.md sec. 5); not the exact order above"}
     return out
 
 

@@ -24,6 +24,8 @@ struct Band2Plan {
   unsigned epoch;
   int kb_up, kb_dn, nk;
   int sys;
+  const short* korder;          // blocked mode (BandPlan of band_sweep.cuh; 16-column bands)
+  const unsigned char* bflags;
 };
 }  // namespace sp
 struct DevCtx;

@@ -183,7 +183,14 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
     if (task >= ntasks || s_stop) return;
     const int s = task / plan.nk;
     const int dir = (int)((plan.dirbits >> (2 * s)) & 3u);
-    const int k = (dir == 0 || dir == 3 ? plan.kb_up : plan.kb_dn) + task % plan.nk;
+    const int frame = dir == 0 || dir == 3 ? 0 : 1;
+    const int k = plan.korder ? (int)plan.korder[frame * plan.nbands + task % plan.nk]
+                              : (frame == 0 ? plan.kb_up : plan.kb_dn) + task % plan.nk;
+    // blocked mode: a block-start band's 2-column halo is OLD, a block-end
+    // band's next two columns (slots B2W, B2W + 1) are NEW
+    const int bfl = plan.bflags ? (int)plan.bflags[frame * plan.nbands + k] : 0;
+    const unsigned hneed = (bfl & 1) ? 0u : 1u;
+    const int hi_slot = (bfl & 2) ? B2W + 2 : 1 << 30;  // (old-ring slot index: +2 for the halo slots)
     BandGeo<ST> b;
     b.nx = f.nx;
     b.ny = f.ny;
@@ -200,9 +207,10 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
 #pragma unroll 1
     for (int t = 0; t < 3; ++t)
       band_load<M, 2>(fa, b, dfirst + t, 0, 18, ep + (unsigned)s, b2_old<M>(smem, dfirst + t) + 2, SPV,
-                      b2_oldp<M>(smem, dfirst + t) + 8, warp, 16, err, kPrologueSleepNs, 0u, sys);
+                      b2_oldp<M>(smem, dfirst + t) + 8, warp, 16, err, kPrologueSleepNs, 0u, sys, hi_slot - 2,
+                      ep + (unsigned)s + 1u);
     if (k > 0 && warp >= 14)
-      band_load<M, 2>(fa, b, dfirst - 1 - (warp - 14), -2, 2, ep + (unsigned)s + 1u,
+      band_load<M, 2>(fa, b, dfirst - 1 - (warp - 14), -2, 2, ep + (unsigned)s + hneed,
                       b2_new<M>(smem, dfirst - 1 - (warp - 14)), SPV, b2_newp<M>(smem, dfirst - 1 - (warp - 14)),
                       0, 1, err, kPrologueSleepNs, 0u, sys);
     if (has_rhs)
@@ -351,7 +359,8 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
         }
         if (wi < 6 && d + 1 <= dlast)
           band_load<M, 3>(fa, b, d + 3, 0, 18, ep + (unsigned)s, b2_old<M>(smem, d + 3) + 2, SPV,
-                          b2_oldp<M>(smem, d + 3) + 8, wi, 6, err, plan.poll_ns, plan.jitter, sys);
+                          b2_oldp<M>(smem, d + 3) + 8, wi, 6, err, plan.poll_ns, plan.jitter, sys, hi_slot - 2,
+                          ep + (unsigned)s + 1u);
         if (has_rhs && wi >= 6 && wi < 10 && d + 1 <= dlast)
           band_load<M, 4>(ra, b, d + 1, 0, B2W, 0u, smem + (LY::V_RHS + ((d + 1) & 1)) * VEC, SPV,
                           smem + LY::PR + ((d + 1) & 1) * 64, wi - 6, 4, err, 0);
@@ -359,7 +368,7 @@ __global__ void __launch_bounds__(THREADS, 1) k6_band(DevField f, DevField rhsf,
           band_pre<M, B2W>(f, ctx, b, d + 1, b2_old<M>(smem, d + 1) + 2, b2_oldp<M>(smem, d + 1) + 8,
                            smem + LY::PRE + ((d + 1) & 1) * PRE_N * 32);
         if (k > 0 && wi == 11 && d + 1 <= dlast)
-          band_load<M, 2>(fa, b, d, -2, 2, ep + (unsigned)s + 1u, b2_new<M>(smem, d), SPV, b2_newp<M>(smem, d),
+          band_load<M, 2>(fa, b, d, -2, 2, ep + (unsigned)s + hneed, b2_new<M>(smem, d), SPV, b2_newp<M>(smem, d),
                           0, 1, err, plan.poll_ns, plan.jitter, sys);
         if (tid == 128) s_stop = stop_now;
       }

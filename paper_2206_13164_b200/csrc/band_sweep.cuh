@@ -192,7 +192,7 @@ __device__ __forceinline__ void band_load(const Addr& fld, const Geo& b, int dd,
   if (lane < MAXS) {
     const int slot = s0 + wi + lane * nw;
     if (slot < s0 + ns) my_cell = b.cell(slot, dd);
-    if (slot == hi_slot) my_need = hi_need;
+    if (slot >= hi_slot) my_need = hi_need;  // (the next band's columns in blocked mode)
   }
   if (jit && need) sched_jitter(jit, (unsigned)dd);
   if (my_need && my_cell >= 0) {

@@ -417,7 +417,7 @@ template <int M>
 constexpr bool use_split() { return M <= 5; }
 unsigned long long* trace_buffer(long long* cap);
 unsigned sched_jitter_seed();
-bool blocked_plan(int T, int nx, const short** korder, const unsigned char** bflags);
+bool blocked_plan(int T, int nx, int band, const short** korder, const unsigned char** bflags);
 void band_scratch(momg_field* f, unsigned** ver, unsigned** next);
 // the band kernels for M <= 5 (momg_set_sweep_mode 1, the default); mode 2
 // runs the thread-per-face / warp-per-cell kernels, mode 0 per-diagonal launches
@@ -489,7 +489,7 @@ struct Launch {
           bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
         }
             bp.jitter = sched_jitter_seed();
-        blocked_plan(ctx.threads, f->nx, &bp.korder, &bp.bflags);
+        blocked_plan(ctx.threads, f->nx, 32, &bp.korder, &bp.bflags);
         const int ndiag = std::min(31, f->nx - 1) + f->ny;
         bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
         bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
@@ -604,7 +604,7 @@ struct Launch {
               bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
             }
             bp.jitter = sched_jitter_seed();
-            blocked_plan(ctx.threads, f->nx, &bp.korder, &bp.bflags);
+            blocked_plan(ctx.threads, f->nx, 32, &bp.korder, &bp.bflags);
             bp.trace = trace_buffer(&bp.trace_cap);
             bp.nchunks = 0;  // no fused residual tasks
             bp.clen = 1;
@@ -625,6 +625,7 @@ struct Launch {
             for (int s = 0; s < 16; ++s) bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
             bp.order = ctx.order;
             bp.has_rhs = rhs != nullptr;
+            blocked_plan(ctx.threads, f->nx, 16, &bp.korder, &bp.bflags);
             bp.jitter = sched_jitter_seed();
             if constexpr (M == 3) band2_launch_m3(fd, rd, c, err, bp, momg_rt::stream());
             else if constexpr (M == 4) band2_launch_m4(fd, rd, c, err, bp, momg_rt::stream());

@@ -474,28 +474,28 @@ unsigned sched_jitter_seed() {
 }
 
 // Blocked-parallel sweep plan (BandPlan::korder / bflags) for T workers on
-// nbands 32-column bands: the reference's blocks [nx b / T, nx (b+1) / T)
+// the nx / band bands (32 columns: k5_band, 16: k6_band): the reference's blocks [nx b / T, nx (b+1) / T)
 // (single_level.cpp:137-141) when every boundary is a band boundary, else
 // null (the exact order, itself one outcome of the reference's blocked run:
-// the workers finishing in block order).  Cached per (T, nx).
-bool blocked_plan(int T, int nx, const short** korder, const unsigned char** bflags) {
+// the workers finishing in block order).  Cached per (T, nx, band).
+bool blocked_plan(int T, int nx, int band, const short** korder, const unsigned char** bflags) {
   *korder = nullptr;
   *bflags = nullptr;
-  if (T <= 1 || nx % 32 || T > nx) return false;
-  const int nb = nx / 32;
+  if (T <= 1 || nx % band || T > nx) return false;
+  const int nb = nx / band;
   std::vector<int> lo(T + 1);
   for (int b = 0; b <= T; ++b) {
     lo[b] = (int)((long long)nx * b / T);
-    if (lo[b] % 32) return false;
+    if (lo[b] % band) return false;
   }
   struct Entry {
-    int T, nx;
+    int T, nx, band;
     short* ko;
     unsigned char* bf;
   };
   static std::vector<Entry> cache;
   for (const Entry& e : cache)
-    if (e.T == T && e.nx == nx) {
+    if (e.T == T && e.nx == nx && e.band == band) {
       *korder = e.ko;
       *bflags = e.bf;
       return true;
@@ -504,7 +504,7 @@ bool blocked_plan(int T, int nx, const short** korder, const unsigned char** bfl
   std::vector<unsigned char> bf(2 * nb, 0);
   for (int fr = 0; fr < 2; ++fr) {
     std::vector<int> rb;  // rotated block boundaries in bands, ascending
-    for (int b = 0; b <= T; ++b) rb.push_back(fr == 0 ? lo[b] / 32 : (nx - lo[T - b]) / 32);
+    for (int b = 0; b <= T; ++b) rb.push_back(fr == 0 ? lo[b] / band : (nx - lo[T - b]) / band);
     int pos = 0;
     for (int t = T - 1; t >= 0; --t) {  // blocks in descending rotated order
       for (int k = rb[t]; k < rb[t + 1]; ++k) ko[fr * nb + pos++] = (short)k;
@@ -514,7 +514,7 @@ bool blocked_plan(int T, int nx, const short** korder, const unsigned char** bfl
       }
     }
   }
-  Entry e{T, nx, nullptr, nullptr};
+  Entry e{T, nx, band, nullptr, nullptr};
   cudaMalloc(&e.ko, ko.size() * sizeof(short));
   cudaMalloc(&e.bf, bf.size());
   cudaMemcpy(e.ko, ko.data(), ko.size() * sizeof(short), cudaMemcpyHostToDevice);
