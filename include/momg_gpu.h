@@ -93,6 +93,8 @@ typedef struct momg_report {
   int history_len;
   double* history;     /* caller buffer, capacity history_cap (nullable) */
   int history_cap;
+  double* history_seconds; /* nullable, capacity history_cap: elapsed seconds at each
+                              iteration (HistoryEntry.seconds, multigrid.cpp:303) */
 } momg_report;
 
 typedef struct momg_field momg_field; /* opaque device-resident level */
@@ -186,6 +188,26 @@ int momg_nmg_cycle_rhs(const momg_ctx* ctx, momg_field* field, const momg_field*
 /* solve_steady: NonConvergence -> MOMG_NONCONVERGENCE with the partial report */
 int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_opts* opts,
                       momg_report* report, momg_err* err);
+
+/* ---- front-end output (scenario.cpp:372-399) ---- */
+/* UnitScales (scenario.hpp:76-84, scenario.cpp:313-319) and GasParams.molecule_mass:
+   lengths scale by `length`, densities by `density`, temperatures (specific-energy
+   form) by `theta`, speeds by `speed`. */
+typedef struct momg_units {
+  double length, density, theta, speed, molecule_mass;
+} momg_units;
+/* export_field's table in laboratory units: per cell, row-major with j outermost,
+   the 11 columns x y rho u1 u2 T sigma11 sigma12 sigma22 q1 q2 (extract_macro,
+   moment_rep.hpp:116-146, evaluated on the device) into the host buffer `out` of
+   nx*ny*11 doubles.  A cell with rho <= 0 is NonphysicalState ("extract_macro:
+   nonpositive density", err->i/j = the first such cell in row order);
+   *rows_ok (nullable) = the rows before it. */
+int momg_field_table(const momg_field* f, const momg_units* u, double* out, long long* rows_ok,
+                     momg_err* err);
+/* export_field (scenario.cpp:372-399): the table as TSV at `path` (header row, values
+   %.17g, tab-separated).  MOMG_ERROR "export_field: cannot open '<path>'" / "write
+   failed"; NonphysicalState after writing the rows before the first rejected cell. */
+int momg_export_field(const momg_field* f, const momg_units* u, const char* path, momg_err* err);
 
 /* ---- strip partition: multi-GPU ------------------ */
 /* A level of `grid` split into n <= 8 column strips [bounds[r], bounds[r+1])

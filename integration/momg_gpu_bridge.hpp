@@ -373,10 +373,11 @@ inline SolveReport solve_steady(CellField& field, const SolveContext& ctx,
   o.s2 = options.cycle.s2;
   o.s3 = options.cycle.s3;
   o.gamma = options.cycle.gamma;
-  std::vector<double> hist(100000);
+  std::vector<double> hist(100000), secs(100000);
   momg_report r{};
   r.history = hist.data();
   r.history_cap = (int)hist.size();
+  r.history_seconds = secs.data();
   momg_err e{};
   const int rc = momg_solve_steady(&c, d.get(), &o, &r, &e);
   SolveReport rep;
@@ -388,7 +389,7 @@ inline SolveReport solve_steady(CellField& field, const SolveContext& ctx,
   rep.work = r.work;
   rep.seconds = r.seconds;
   for (int k = 0; k < r.history_len && k < r.history_cap; ++k)
-    rep.history.push_back({k + 1, hist[k], 0.0});
+    rep.history.push_back({k + 1, hist[k], secs[k]});
   download(d.get(), field);
   if (rc != MOMG_OK) rethrow(rc, e, &rep);
   return rep;

@@ -5,6 +5,7 @@
 // reference's types (CellField / MomentRep / Grid2D, grid.hpp:12-85), calls the
 // reference function named in its comment, and maps its exceptions onto
 // mo_err codes.  No arithmetic of the path happens here.
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -16,6 +17,7 @@
 #include "momg/hermite.hpp"
 #include "momg/multigrid.hpp"
 #include "momg/projection.hpp"
+#include "momg/scenario.hpp"
 #include "momg/single_level.hpp"
 #include "momg/spatial.hpp"
 #include "momg_oracle.h"
@@ -440,6 +442,33 @@ int mo_euler_step_rhs(const mo_ctx* ctx, const mo_grid* g, double* coeffs, doubl
   });
   put_field(f, coeffs, params);
   return rc;
+}
+
+
+// ---- front end (scenario.cpp), reference only: golden fixtures of the wire formats
+// parse_config (scenario.cpp:219-311) + config_echo (:321-352) of a JSON document
+int mo_ref_config_echo(const char* json_text, char* out, int cap, mo_err* err) {
+  return guarded(err, [&] {
+    const std::string e = config_echo(parse_config(json_text));
+    std::snprintf(out, (size_t)cap, "%s", e.c_str());
+    if ((int)e.size() >= cap) throw Error("mo_ref_config_echo: buffer too small");
+  });
+}
+
+// run_scenario (scenario.cpp:401-459) of a JSON document: writes history.tsv,
+// field.tsv and report.txt under its output_dir
+int mo_ref_run_scenario(const char* json_text, mo_err* err) {
+  return guarded(err, [&] { run_scenario(parse_config(json_text)); });
+}
+
+// export_field (scenario.cpp:372-399) of a given field with the unit scales of a
+// JSON document's configuration
+int mo_ref_export_field(const char* json_text, const mo_grid* g, int M, const double* coeffs,
+                        const double* params, const char* path, mo_err* err) {
+  return guarded(err, [&] {
+    const ScenarioConfig c = parse_config(json_text);
+    export_field(field(grid(g), M, coeffs, params), c, unit_scales(c), path);
+  });
 }
 
 }  // extern "C"

@@ -417,6 +417,7 @@ int momg_solve_steady(const momg_ctx* ctx, momg_field* field, const momg_solver_
       rep.iterations = n;
       rep.final_ratio = rep.final_norm / rep.r0_norm;
       if (rep.history && rep.history_len < rep.history_cap) rep.history[rep.history_len] = rep.final_ratio;
+      if (rep.history_seconds && rep.history_len < rep.history_cap) rep.history_seconds[rep.history_len] = elapsed();
       rep.history_len++;
       rep.work = work;
       rep.seconds = elapsed();

@@ -102,7 +102,8 @@ class _Report(C.Structure):
     _fields_ = [("converged", C.c_int), ("iterations", C.c_int), ("r0_norm", C.c_double),
                 ("final_norm", C.c_double), ("final_ratio", C.c_double), ("work", C.c_longlong),
                 ("seconds", C.c_double), ("history_len", C.c_int),
-                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int)]
+                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int),
+                ("history_seconds", C.POINTER(C.c_double))]
 
 
 _lib = None
@@ -303,6 +304,7 @@ class SolveReport:
     work: int = 0
     seconds: float = 0.0
     history: list = field(default_factory=list)
+    history_seconds: list = field(default_factory=list)  # HistoryEntry.seconds
 
 
 def count(order: int) -> int:
@@ -503,15 +505,44 @@ def solve_steady(field: CellField, ctx: SolveContext, options: SolverOptions,
     o = _Opts(int(options.kind), options.tol, options.max_iterations, options.levels,
               options.cycle.s1, options.cycle.s2, options.cycle.s3, options.cycle.gamma)
     hist = np.zeros(history_cap)
-    rep = _Report(0, 0, 0.0, 0.0, 0.0, 0, 0.0, 0, _dp(hist), history_cap)
+    secs = np.zeros(history_cap)
+    rep = _Report(0, 0, 0.0, 0.0, 0.0, 0, 0.0, 0, _dp(hist), history_cap, _dp(secs))
     rc = lib().momg_solve_steady(C.byref(c), field._h, C.byref(o), C.byref(rep), C.byref(err))
+    n = min(rep.history_len, history_cap)
     report = SolveReport(bool(rep.converged), rep.iterations, rep.r0_norm, rep.final_norm,
-                         rep.final_ratio, rep.work, rep.seconds,
-                         list(hist[:min(rep.history_len, history_cap)]))
+                         rep.final_ratio, rep.work, rep.seconds, list(hist[:n]), list(secs[:n]))
     if rc == 6:
         raise NonConvergence(err.msg.decode(errors="replace"), report)
     _raise(rc, err)
     return report
+
+
+# --------------------------------------------------------- front-end output
+class _Units(C.Structure):
+    _fields_ = [("length", C.c_double), ("density", C.c_double), ("theta", C.c_double),
+                ("speed", C.c_double), ("molecule_mass", C.c_double)]
+
+
+def field_table(field: CellField, length: float, density: float, theta: float, speed: float,
+                molecule_mass: float) -> np.ndarray:
+    """export_field's table (scenario.cpp:372-399) evaluated on the device: per cell,
+    row-major with j outermost, x y rho u1 u2 T sigma11 sigma12 sigma22 q1 q2 in
+    laboratory units (momg_field_table).  NonphysicalState at a cell with rho <= 0."""
+    out = np.empty((field.size(), 11))
+    err = _Err()
+    u = _Units(length, density, theta, speed, molecule_mass)
+    rows = C.c_longlong(0)
+    _raise(lib().momg_field_table(field._h, C.byref(u), _dp(out), C.byref(rows), C.byref(err)), err)
+    return out
+
+
+def export_field_tsv(field: CellField, path: str, length: float, density: float, theta: float,
+                     speed: float, molecule_mass: float) -> None:
+    """export_field (scenario.cpp:372-399): the table as TSV (%.17g) at path
+    (momg_export_field; the formatting runs in the library on all host threads)."""
+    err = _Err()
+    u = _Units(length, density, theta, speed, molecule_mass)
+    _raise(lib().momg_export_field(field._h, C.byref(u), os.fsencode(path), C.byref(err)), err)
 
 
 # ------------------------------------------------------------------ strips

@@ -268,11 +268,12 @@ def test_nmg_and_solve_bitwise(R):
 @needs_ref
 def test_reference_unit_tests():
     """The reference's own doctest suites pass against the shims (validates the
-    Eigen/doctest shims that oracle/_ref is built with)."""
+    Eigen / doctest / nlohmann-json shims that oracle/_ref is built with; the
+    scenario suite runs the front end, scenario.cpp, including one NMG solve)."""
     if not os.path.isdir("/root/reference/proj"):
         pytest.skip("reference sources absent")
     here = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle")
     out = subprocess.run(["make", "-s", "-C", here, "ref-tests"], capture_output=True, text=True,
                          timeout=900)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
-    assert out.stdout.count("| 0 failed") == 8
+    assert out.stdout.count("| 0 failed") == 9
