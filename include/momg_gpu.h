@@ -257,6 +257,12 @@ int momg_strips_scatter(momg_strips* s, int which, const momg_field* full, momg_
    the band kernels (thread-per-face / warp-per-cell for every M); 0: one launch
    per anti-diagonal (the simple reference strategy; env MOMG_SWEEP=diag). */
 int momg_set_sweep_mode(int mode);
+/* band kernel of the first-order exact sweeps and residuals (M <= 5): 1
+   (default; env MOMG_RB=0 selects 0) the register-resident kernel (one thread
+   per face side, moment vectors in registers); 0 the split kernel (each face
+   cut 4 ways across warps through shared memory).  Results agree to rounding
+   (the two halves of a face flux are summed after the back projection). */
+int momg_set_band_kernel(int kind);
 
 /* ---- instrumentation --------------------------------------------------- */
 /* debug: %globaltimer stamps of the first cap band tasks of the band sweep

@@ -22,6 +22,7 @@
 #include "kernels_v3.cuh"
 #include "split_cell.cuh"
 #include "band_sweep.cuh"
+#include "reg_band.cuh"
 #include "transfer.cuh"
 #include "band2.h"
 
@@ -422,6 +423,26 @@ void band_scratch(momg_field* f, unsigned** ver, unsigned** next);
 // the band kernels for M <= 5 (momg_set_sweep_mode 1, the default); mode 2
 // runs the thread-per-face / warp-per-cell kernels, mode 0 per-diagonal launches
 bool band_sweep_enabled();
+// the register-resident band kernel (reg_band.cuh) for first-order exact
+// sweeps / residuals of M <= 5 (momg_set_band_kernel: 1 default, 0 k5_band)
+bool rb_enabled();
+
+// launch of rb::k8_band (grid: one CTA per SM, at most one per task)
+template <int M, bool RES>
+void rb_launch(const DevField& f, const DevCtx& ctx, const sp::BandPlan& bp, const DevField& out) {
+  static bool attr = false;
+  if (!attr) {
+    set_smem(rb::k8_band<M, RES>, rb::RLayout<M>::bytes);
+    attr = true;
+  }
+  int nb = tc_sweep_blocks((const void*)rb::k8_band<M, RES>, rb::RLayout<M>::bytes, rb::RT);
+  const int tasks = (RES ? 0 : bp.nsweeps * bp.nk) + bp.nchunks * bp.nk;
+  if (nb > tasks) nb = tasks;
+  if (nb < 1) nb = 1;
+  rb::k8_band<M, RES><<<nb, rb::RT, rb::RLayout<M>::bytes, momg_rt::stream()>>>(f, ctx, momg_rt::err_dev(), bp,
+                                                                                   out);
+  momg_rt::count_launch(1);
+}
 
 // ---------------------------------------------------- templated launchers
 template <int M>
@@ -494,6 +515,10 @@ struct Launch {
         bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
         bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
         bp.nchunks = (ndiag + bp.clen - 1) / bp.clen;
+        if (rb_enabled() && !bp.korder) {
+          rb_launch<M, false>(f->dev(), ctx, bp, out->dev());
+          return true;
+        }
         int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
         const int tasks = (bp.nsweeps + bp.nchunks) * bp.nbands;
         if (nb > tasks) nb = tasks;
@@ -529,6 +554,10 @@ struct Launch {
         bp.nchunks = std::max(1, (2 * 148 + bp.nbands - 1) / bp.nbands);
         bp.clen = (ndiag + bp.nchunks - 1) / bp.nchunks;
         bp.nchunks = (ndiag + bp.clen - 1) / bp.clen;
+        if (rb_enabled()) {
+          rb_launch<M, true>(f->dev(), ctx, bp, out->dev());
+          return;
+        }
         const int tasks = bp.nbands * bp.nchunks;
         const int nb = tasks < 148 ? tasks : 148;
         DevCtx c = ctx;
@@ -608,6 +637,10 @@ struct Launch {
             bp.trace = trace_buffer(&bp.trace_cap);
             bp.nchunks = 0;  // no fused residual tasks
             bp.clen = 1;
+            if (rb_enabled() && !bp.korder) {
+              rb_launch<M, false>(fd, c, bp, fd);
+              return;
+            }
             int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
             if (nb > bp.nsweeps * bp.nbands) nb = bp.nsweeps * bp.nbands;
             sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp, fd);

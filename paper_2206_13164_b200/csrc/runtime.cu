@@ -403,6 +403,7 @@ bool persistent_sweep_enabled() {
 }
 void set_sweep_mode(int m) { g_sweep_mode = m; }
 void set_band_mode(int m);
+void set_rb_mode(int m);
 void set_trace(long long cap);
 long long read_trace(unsigned long long* host, long long n);
 
@@ -538,6 +539,16 @@ void band_scratch(momg_field* f, unsigned** ver, unsigned** next) {
 static int g_band = 1;
 bool band_sweep_enabled() { return g_band == 1 && persistent_sweep_enabled(); }
 void set_band_mode(int m) { g_band = m; }
+// register-resident band kernel (reg_band.cuh) vs the split k5_band
+static int g_rb = -1;
+bool rb_enabled() {
+  if (g_rb < 0) {
+    const char* e = getenv("MOMG_RB");
+    g_rb = (e && std::string(e) == "0") ? 0 : 1;
+  }
+  return g_rb == 1;
+}
+void set_rb_mode(int m) { g_rb = m; }
 
 int tc_sweep_blocks(const void* kernel, size_t smem, int threads) {
   int per_sm = 0, dev = 0, sms = 0;
@@ -788,6 +799,12 @@ int momg_set_sweep_mode(int mode) {
   if (mode < 0 || mode > 2) return MOMG_ERR_ARG;
   momg_gpu::set_sweep_mode(mode == 0 ? 0 : 1);
   momg_gpu::set_band_mode(mode == 1 ? 1 : 0);
+  return MOMG_OK;
+}
+
+int momg_set_band_kernel(int kind) {
+  if (kind < 0 || kind > 1) return MOMG_ERR_ARG;
+  momg_gpu::set_rb_mode(kind);
   return MOMG_OK;
 }
 

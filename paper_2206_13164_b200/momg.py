@@ -722,3 +722,13 @@ def set_sweep_mode(mode: str) -> None:
     rc = lib().momg_set_sweep_mode({"diag": 0, "persistent": 1, "warp": 2}[mode])
     if rc:
         raise ValueError(mode)
+
+
+def set_band_kernel(kind: str) -> None:
+    """Band kernel of the first-order exact sweeps and residuals (M <= 5):
+    'register' (default: one thread per face side, moment vectors in
+    registers) or 'split' (each face cut 4 ways across warps through shared
+    memory).  Results agree to rounding."""
+    rc = lib().momg_set_band_kernel({"split": 0, "register": 1}[kind])
+    if rc:
+        raise ValueError(kind)

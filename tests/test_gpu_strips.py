@@ -6,7 +6,10 @@ cross-strip halo cells and counters are read in the neighbouring strip's
 memory exactly as a peer rank's would be over NVLink.  Required: bitwise
 equality with the single-field fused FS + residual (and, through it, the
 oracle), over consecutive calls (counter epochs), several strip layouts,
-sweep orders and schedule perturbations."""
+sweep orders and schedule perturbations.  The strip partition runs the split
+band kernel (k5_band's strips variant), so the single-field reference here
+runs the split kernel too (momg.set_band_kernel("split")); the default
+register-resident kernel agrees with it to rounding (test_gpu_rb.py)."""
 import os
 
 import numpy as np
@@ -18,6 +21,13 @@ from test_gpu_parity import mctx, mgrid, rel_field, rel_res
 pytestmark = pytest.mark.gpu
 
 momg = pytest.importorskip("paper_2206_13164_b200.momg")
+
+
+@pytest.fixture(autouse=True)
+def split_band_kernel():
+    momg.set_band_kernel("split")
+    yield
+    momg.set_band_kernel("register")
 
 CASES = [
     # (M, model, nx, ny, bounds, sweep order)

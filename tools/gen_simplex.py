@@ -19,6 +19,7 @@ Generated per M (struct Gen<M>):
                        in place into L: out(beta) = sum_m L(beta|m) Ku[m][p] + R(beta|m) Kl[m][p]
                        (flux.cpp:58-73 with folded kernels), p = beta_a
   half_one<a>(L, K)    single-sided variant (wall outgoing flux)
+  half_sr<a>(s, o, K)  single-sided, strided source -> separate output
   full_flux<a>(src, dst, un, th)
                        flux.cpp:10-27
 Usage: python tools/gen_simplex.py  (writes the header; run by csrc/Makefile)
@@ -103,10 +104,35 @@ def emit_order(M):
                     w(f"      Lv[{k} * VS] = {expr};")
                 w("    }")
             w("  }")
+    # half flux of one side from a strided source into a separate output
+    # (register-resident band kernel): longest pencils first, so the
+    # kernel entries of the long pencils die before the output fills up
+    for a in range(2):
+        w(f"  // single-side half-space flux along axis {a}: o = K applied to s (pencils by decreasing length)")
+        w(f"  template <int VS, int VO>")
+        w(f"  static __device__ __forceinline__ void half_sr{a}(const double* __restrict__ s, double* __restrict__ o, const double (&K)[{M + 1}][{M + 1}]) {{")
+        tans = {}
+        for b in idx:
+            t = tuple(b[o] for o in range(3) if o != a)
+            tans.setdefault(t, []).append(b)
+        for t, members in sorted(tans.items(), key=lambda tm: -len(tm[1])):
+            members.sort(key=lambda b: b[a])
+            ks = [pos[b] for b in members]
+            n = len(ks)
+            w("    {")
+            for m, k in enumerate(ks):
+                w(f"      const double l{m} = s[{k} * VS];")
+            for p, k in enumerate(ks):
+                expr = "0.0"
+                for m in range(n):
+                    expr = f"fma(l{m}, K[{m}][{p}], {expr})" if expr != "0.0" else f"l{m} * K[{m}][{p}]"
+                w(f"      o[{k} * VO] = {expr};")
+            w("    }")
+        w("  }")
     # ------------------------------------------------------------ full flux
     for a in range(2):
         w(f"  // full-space flux xi_{a} f (flux.cpp:10-27), closure drops degree M+1")
-        w(f"  template <int VS>")
+        w(f"  template <int VS, int VO = VS>")
         w(f"  static __device__ __forceinline__ void full_flux{a}(const double* __restrict__ s, double* __restrict__ o, double un, double th) {{")
         for b in idx:
             k = pos[b]
@@ -117,7 +143,7 @@ def emit_order(M):
             if sum(b) < M:
                 up = list(b); up[a] += 1
                 expr = f"fma({float(b[a] + 1)}, s[{pos[tuple(up)]} * VS], {expr})"
-            w(f"    o[{k} * VS] = {expr};")
+            w(f"    o[{k} * VO] = {expr};")
         w("  }")
     # Shakhov eq pattern: positions of 2 e_dd + e_d and the q components
     w("  // Shakhov equilibrium positions (collision.hpp:95-111): 3 e_d and e_d + 2 e_dd")
