@@ -110,13 +110,16 @@ class Clocks:
 
 def band_traffic(nx):
     """DRAM bytes (read + write) per launch of the band sweep measured by ncu at
-    this grid size (profiles/r1_band_traffic.json, from tools/profile.sh), or None."""
-    path = os.path.join(ROOT, "profiles", "r1_band_traffic.json")
-    try:
-        d = json.load(open(path))
-        return d["bytes_per_launch"] if d.get("nx") == nx else None
-    except (OSError, ValueError, KeyError):
-        return None
+    this grid size (profiles/r2_k8_traffic.json, from tools/profile_k8.sh; the
+    round-1 figure of the split kernel as the fallback), or None."""
+    for name in ("r2_k8_traffic.json", "r1_band_traffic.json"):
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", name)))
+            if d.get("nx") == nx:
+                return d["bytes_per_launch"]
+        except (OSError, ValueError, KeyError):
+            pass
+    return None
 
 
 def fp64_peak():
@@ -376,7 +379,7 @@ def ours(a):
     kflops = FLOPS_PER_UPDATE_C5 * updates + (FLOPS_RESIDUAL_C5 * nx * nx if FUSED else 0.0)
     achieved = kflops / (sweep_med * 1e-3) / 1e12
     roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": band_traffic(nx), "kernel": "sp::k5_band<5,32>",
+            "frac": achieved / peak, "traffic": band_traffic(nx), "kernel": "rb::k8_band<5>" if a.order == 1 else "sp::k6_band<5>",
             "flops_per_update": FLOPS_PER_UPDATE_C5,
             "flops_per_launch": kflops, "fused_residual": FUSED, "peak_source": peak_src,
             "kernel_ms": sweep_med,

@@ -47,14 +47,15 @@ template <int M>
 struct RLayout {
   static constexpr int N = Gen<M>::N;
   static constexpr int VEC = N * SPV;
-  // vectors: O[3] old-state ring (O[d % 3] = old(d), 33 slots: the band's 32
-  // columns + band k+1's first), V[2] new states (V[d & 1]), F[8] face sides
-  // (F[0] doubles as the assembled residual D).  Band k-1's halo cell of a
-  // diagonal lives in slot 32 of that diagonal's upstream vector (V of the
-  // sweep, O of the residual), which is free once the diagonal is upstream.
-  static constexpr int V_O = 0, V_V = 3, V_F = 5, NV = 13;
-  static constexpr int PO = NV * VEC;      // [3][33][4]
-  static constexpr int PV = PO + 3 * 132;  // [2][33][4]
+  // vectors: O[4] old-state ring (O[d & 3] = old(d), 33 slots: the band's 32
+  // columns + band k+1's first; old(d), old(d+1) in use, old(d+2) landed,
+  // old(d+3) in flight as cp.async), V[2] new states (V[d & 1]), F[8] face
+  // sides (F[0] doubles as the assembled residual D).  Band k-1's halo cell
+  // of a diagonal lives in slot 32 of that diagonal's upstream vector (V of
+  // the sweep, O of the residual), which is free once the diagonal is upstream.
+  static constexpr int V_O = 0, V_V = 4, V_F = 6, NV = 14;
+  static constexpr int PO = NV * VEC;      // [4][33][4]
+  static constexpr int PV = PO + 4 * 132;  // [2][33][4]
   static constexpr int PRE = PV + 2 * 132;  // [2][PRE_N][32]
   static constexpr size_t bytes = (size_t)(PRE + 2 * sp::PRE_N * 32) * sizeof(double);
 };
@@ -84,9 +85,10 @@ __device__ __forceinline__ void half_kernel_side(double un, double rs, const tc:
   for (int p = 0; p <= M; ++p) {
     double col[P + 1];
     col[0] = p == 0 ? hb.e0 : he[p - 1] * g;
+    const double hpg = he[p] * g;
 #pragma unroll
     for (int m = 0; m + 1 <= P; ++m) {
-      const double t = he[m] * he[p] * g;
+      const double t = he[m] * hpg;
       col[m + 1] = p > 0 ? fma((double)p, prev[m], t) : t;
     }
     if (p > 0) {
@@ -96,15 +98,13 @@ __device__ __forceinline__ void half_kernel_side(double un, double rs, const tc:
     double scale = rsp * kInvFact[p];
 #pragma unroll
     for (int m = 0; m <= M; ++m) {
-      const double lo_m = (m == p ? fp : 0.0) - col[m];
-      const double lo_p1 = (m + 1 == p ? fp : 0.0) - col[m + 1];
+      // upper table: ku; the lower one is the full-space (tridiagonal) kernel minus ku
       double ku = fma(un, col[m], rs * col[m + 1]);
-      double kl = fma(un, lo_m, rs * lo_p1);
-      if (m > 0) {
-        const double lo_m1 = (m - 1 == p ? fp : 0.0) - col[m - 1];
-        ku = fma(rs * (double)m, col[m - 1], ku);
-        kl = fma(rs * (double)m, lo_m1, kl);
-      }
+      if (m > 0) ku = fma(rs * (double)m, col[m - 1], ku);
+      double kl = -ku;
+      if (m == p) kl = fma(un, fp, -ku);
+      else if (m + 1 == p) kl = fma(rs, fp, -ku);
+      else if (m - 1 == p) kl = fma(rs * (double)m, fp, -ku);
       K[m][p] = scale * (upper ? ku : kl);
       if (m == 0) kin0[p] = scale * (upper ? kl : ku);
       scale *= irs;
@@ -300,6 +300,85 @@ __device__ __forceinline__ void assemble_part(int w, const double* S, const doub
 #undef RB_AS
 }
 
+// Asynchronous variant of sp::band_load: warp wi of nw polls the counters of
+// its slots of diagonal dd (one lane per slot), then issues 8-byte cp.async
+// copies (lane = coefficient: coalesced in HBM, transposed into
+// vec[k * SPV + slot] on the way) and returns without waiting; the caller
+// waits (cp_async_wait) before a CTA barrier one step later.  Slots outside
+// the grid are zero-filled with plain stores.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Wait until the cell's counter reaches `need`: one acquire load when it
+// already has (the common case: one round trip), else relaxed polling with
+// back-off and a final acquire.
+__device__ __forceinline__ void poll_acquire(const unsigned* a, unsigned need, int cell, int nx, DevErr* err,
+                                             int poll_ns) {
+  if (ld_acquire_s(a, false) >= need) return;
+  long long polls = 0;
+  while (ld_relaxed_s(a, false) < need) {
+    if (sp::band_stop(err)) break;
+    if (++polls > (1LL << 26)) {
+      tc::raise(err, E_ERROR, W_DEADLOCK, cell % nx, cell / nx, (double)need);
+      break;
+    }
+    if (poll_ns) __nanosleep(poll_ns);
+  }
+  (void)ld_acquire_s(a, false);
+}
+
+template <int M, int MAXS, class Addr, class Geo>
+__device__ __forceinline__ void band_load_async(const Addr& fld, const Geo& b, int dd, int ns, unsigned need,
+                                                double* vec, double* prm, int wi, int nw, DevErr* err, int poll_ns,
+                                                unsigned jit, unsigned ahead) {
+  constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, H = (N + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  int my_cell = -1;
+  if (lane < MAXS) {
+    const int slot = wi + lane * nw;
+    if (slot < ns) my_cell = b.cell(slot, dd);
+  }
+  if (jit && need) sp::sched_jitter(jit, (unsigned)dd);
+  // `ahead`: this lane's counter of diagonal dd as the previous step's acquire load saw it
+  if (need && my_cell >= 0 && ahead < need) poll_acquire(fld.vptr(my_cell), need, my_cell, b.nx, err, poll_ns);
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < MAXS; ++t) {
+    const int slot = wi + t * nw;
+    if (slot >= ns) continue;
+    const int cl = __shfl_sync(0xffffffffu, my_cell, t);
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int kk = lane + 32 * h;
+      if (kk < N) {
+        if (cl >= 0) cp_async8(vec + kk * SPV + slot, fld.cptr(cl, NP) + kk);
+        else vec[kk * SPV + slot] = 0.0;
+      }
+    }
+    if (lane < 4) {
+      if (cl >= 0) cp_async8(prm + slot * 4 + lane, fld.pptr(cl) + lane);
+      else prm[slot * 4 + lane] = 0.0;
+    }
+  }
+}
+// the acquire load of a diagonal's counters (the lane -> slot map of
+// band_load_async), one step ahead of their use
+template <int MAXS, class Addr, class Geo>
+__device__ __forceinline__ unsigned band_counters_ahead(const Addr& fld, const Geo& b, int dd, int ns, unsigned need,
+                                                        int wi, int nw) {
+  const int lane = threadIdx.x & 31;
+  unsigned ahead = 0u;
+  if (need && lane < MAXS) {
+    const int slot = wi + lane * nw;
+    const int nc = slot < ns ? b.cell(slot, dd) : -1;
+    if (nc >= 0) ahead = ld_acquire_s(fld.vptr(nc), false);
+  }
+  return ahead;
+}
+
 // Coalesced write-back of nc cells starting at c0 of diagonal dd (new states
 // V[dd & 1], bases PV, only cells whose update succeeded); lane = coefficient.
 template <int M, class Geo>
@@ -338,7 +417,10 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
   constexpr int N = LY::N, VEC = LY::VEC, NP = (N + 3) & ~3;
   extern __shared__ __align__(128) double smem[];
   __shared__ int s_task, s_stop;
-  __shared__ int s_ok[32];
+  __shared__ int s_ok[2][32];
+  // debug trace accumulators: [0] step start, [1] write-back, [2] faces, [3] assembled, [4] updated, [5] end;
+  // s_wA / s_wC: per-warp arrival at the face / end-of-step barrier
+  __shared__ unsigned long long s_tr[6], s_wA[8], s_wC[8], s_wM[8];
   const int tid = threadIdx.x, warp = tid >> 5, c = tid & 31;
   const int sweep_tasks = RES ? 0 : plan.nsweeps * plan.nk;
   const int ntasks = sweep_tasks + plan.nchunks * plan.nk;
@@ -379,8 +461,14 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
         continue;
       }
     }
-    const bool tr = plan.trace && 4 * task + 3 < plan.trace_cap && tid == 0;
+    const bool trw = plan.trace && 4 * task + 3 < plan.trace_cap && c == 0;
+    const bool tr = trw && tid == 0;
     unsigned long long t0 = 0;
+    if (trw) {
+      s_wA[warp] = s_wC[warp] = s_wM[warp] = 0;
+      if (tid == 0)
+        for (int q = 0; q < 6; ++q) s_tr[q] = 0;
+    }
     // ---- prologue: warp 0 waits (with back-off) for the first two diagonals
     // and band k-1's halo cell; then O <- old(dfirst), old(dfirst+1), halo
     if (!res && warp == 0) {
@@ -404,22 +492,24 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
     }
     __syncthreads();
     const unsigned pn = res ? rneed : 0u;
-    sp::band_load<M, 5>(fa, b, dfirst, 0, NS, pn, O + (dfirst % 3) * VEC, SPV, PO + (dfirst % 3) * 132, warp, 8,
+    sp::band_load<M, 5>(fa, b, dfirst, 0, NS, pn, O + (dfirst & 3) * VEC, SPV, PO + (dfirst & 3) * 132, warp, 8,
                         err, sp::kPrologueSleepNs);
-    sp::band_load<M, 5>(fa, b, dfirst + 1, 0, NS, pn, O + ((dfirst + 1) % 3) * VEC, SPV,
-                        PO + ((dfirst + 1) % 3) * 132, warp, 8, err, sp::kPrologueSleepNs);
+    sp::band_load<M, 5>(fa, b, dfirst + 1, 0, NS, pn, O + ((dfirst + 1) & 3) * VEC, SPV,
+                        PO + ((dfirst + 1) & 3) * 132, warp, 8, err, sp::kPrologueSleepNs);
+    sp::band_load<M, 5>(fa, b, dfirst + 2, 0, NS, res ? rneed : ep + (unsigned)s, O + ((dfirst + 2) & 3) * VEC, SPV,
+                        PO + ((dfirst + 2) & 3) * 132, warp, 8, err, sp::kPrologueSleepNs);
     if (res)  // a chunk may start mid-band: its upstream states are old(dfirst-1)
-      sp::band_load<M, 4>(fa, b, dfirst - 1, 0, BW, pn, O + ((dfirst + 2) % 3) * VEC, SPV,
-                          PO + ((dfirst + 2) % 3) * 132, warp, 8, err, sp::kPrologueSleepNs);
+      sp::band_load<M, 4>(fa, b, dfirst - 1, 0, BW, pn, O + ((dfirst + 3) & 3) * VEC, SPV,
+                          PO + ((dfirst + 3) & 3) * 132, warp, 8, err, sp::kPrologueSleepNs);
     if (k > 0 && warp == 7)
       sp::band_load<M, 1>(fa, b, dfirst - 1, -1, 1, pn,
-                          (res ? O + ((dfirst + 2) % 3) * VEC : smem + (LY::V_V + ((dfirst - 1) & 1)) * VEC) + 32,
-                          SPV, (res ? PO + ((dfirst + 2) % 3) * 132 : smem + LY::PV + ((dfirst - 1) & 1) * 132) + 128,
+                          (res ? O + ((dfirst + 3) & 3) * VEC : smem + (LY::V_V + ((dfirst - 1) & 1)) * VEC) + 32,
+                          SPV, (res ? PO + ((dfirst + 3) & 3) * 132 : smem + LY::PV + ((dfirst - 1) & 1) * 132) + 128,
                           0, 1, err,
                           sp::kPrologueSleepNs);
     __syncthreads();
     if (warp == 1)
-      sp::band_pre<M, BW>(f, ctx, b, dfirst, O + (dfirst % 3) * VEC, PO + (dfirst % 3) * 132,
+      sp::band_pre<M, BW>(f, ctx, b, dfirst, O + (dfirst & 3) * VEC, PO + (dfirst & 3) * 132,
                           smem + LY::PRE + (dfirst & 1) * sp::PRE_N * 32);
     __syncthreads();
     if (tr) t0 = sp::gtimer();
@@ -432,12 +522,11 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
     // F pointers of the assembly: [x high side0, side1, x low ..., y high ..., y low ...]
     const bool xu_high = !b.i_up, yu_high = !b.j_up;
     const int fxh = xu_high ? 0 : 1, fyh = yu_high ? 2 : 3;
+    unsigned ahead = 0u;  // warps 5, 6: the counters of the next diagonal to copy, read one step ahead
     for (int d = dfirst; d <= dlast; ++d) {
-      const int o0 = d % 3, o1 = (d + 1) % 3, om = (d + 2) % 3;  // old(d), old(d+1), old(d-1) / old(d+2)
-      // write-back of step d-1 (its release follows the next CTA barrier)
-      if (!res && d > dfirst)
-        rb_writeback<M>(f, b, d - 1, smem + (LY::V_V + ((d - 1) & 1)) * VEC, smem + LY::PV + ((d - 1) & 1) * 132,
-                        s_ok, 4 * warp, 4);
+      // old(d), old(d+1); om: old(d-1) (residual tasks) until phase (C) starts the copy of old(d+3) into it
+      const int o0 = d & 3, o1 = (d + 1) & 3, om = (d + 3) & 3;
+      if (tr) s_tr[0] = sp::gtimer();
       // ---- (A) faces: this warp's side of its face for the 32 cells
       const int jr = d - ir;
       const bool valid = ir < f.nx && jr >= 0 && jr < f.ny;
@@ -473,7 +562,9 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
           tc::raise(err, tc::code_for(w), w, i, j, 0.0);
         }
       }
+      if (trw) s_wA[warp] += sp::gtimer() - s_tr[0];
       __syncthreads();
+      if (tr) s_tr[2] += sp::gtimer() - s_tr[0];
       // ---- (B) residual assembly, coefficients split over the 8 warps (D in F[0])
       const double* pre = smem + LY::PRE + (d & 1) * sp::PRE_N * 32 + c;
       const int pfail = valid ? (int)pre[sp::PRE_FAIL * 32] : W_NONE;
@@ -490,6 +581,7 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
         }
       }
       __syncthreads();
+      if (tr) s_tr[3] += sp::gtimer() - s_tr[0];
       // ---- (C) warp 0: the cell update (sweep) / the residual stores (res);
       // the others: publish d-1, scalars of d+1, old(d+2), band k-1's halo
       if (warp == 0 && !res) {
@@ -535,7 +627,8 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
 #pragma unroll
           for (int t = 0; t < 4; ++t) pv[t] = prm.v[t];
         }
-        s_ok[c] = ok ? 1 : 0;
+        s_ok[d & 1][c] = ok ? 1 : 0;
+        if (tr) s_tr[4] += sp::gtimer() - s_tr[0];
       } else if (res && warp <= 1) {
         // residual: coalesced store of D (lane = coefficient), 16 cells per warp
         const double* Db = smem + LY::V_F * VEC;
@@ -560,40 +653,81 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
           tc::raise(err, tc::code_for(pfail), pfail, i, j, 0.0);
         }
       } else if (warp == 1) {
-        // publish step d-1 (written back before the last CTA barrier), then
-        // the update scalars of d+1 (old(d+1) has been in O since step d-1)
-        if (d > dfirst) {
-          sp::sched_jitter(plan.jitter, (unsigned)d);
-          const int cl = b.cell(c, d - 1);
-          if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, false);
-        }
+        // the update scalars of d+1 (old(d+1) has been in O since step d-2)
         if (d + 1 <= dlast)
           sp::band_pre<M, BW>(f, ctx, b, d + 1, O + o1 * VEC, PO + o1 * 132,
                               smem + LY::PRE + ((d + 1) & 1) * sp::PRE_N * 32);
-      } else if (warp >= 2 && warp <= 6) {
+      } else {  // warps 2..7
         const int stop_now = warp == 2 && c == 0 ? sp::band_stop(err) : 0;
-        if (d + 1 <= dlast)
-          sp::band_load<M, 7>(fa, b, d + 2, 0, NS, res ? rneed : ep + (unsigned)s, O + om * VEC, SPV,
-                              PO + om * 132, warp - 2, 5, err, plan.poll_ns, plan.jitter, false);
+        // every role below is one or two dependent memory round trips, shorter than warp 0's update
+        if (warp <= 4) {
+          // publication of step d-2 (its stores were issued a step ago: the
+          // release has nothing to wait for), then the write-back of step d-1
+          // (final since the last CTA barrier); a contiguous third of the 32
+          // cells per warp
+          if (!res && d > dfirst) {
+            const int wq = warp - 2, c0 = 11 * wq, nc = wq < 2 ? 11 : 10;
+            sp::sched_jitter(plan.jitter, (unsigned)d);
+            if (d - 2 >= dfirst && c < nc) {
+              const int cl = b.cell(c0 + c, d - 2);
+              if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, false);
+            }
+            if (trw) s_wM[warp] += sp::gtimer() - s_tr[0];
+            rb_writeback<M>(f, b, d - 1, smem + (LY::V_V + ((d - 1) & 1)) * VEC, smem + LY::PV + ((d - 1) & 1) * 132,
+                            s_ok[(d - 1) & 1], c0, nc);
+            __syncwarp();
+          }
+        } else if (warp <= 6) {
+          // old(d+2), issued one step ago, has landed; start the copy of old(d+3)
+          cp_async_wait();
+          if (d + 2 <= dlast) {
+            const unsigned need = res ? rneed : ep + (unsigned)s;
+            band_load_async<M, 17>(fa, b, d + 3, NS, need, O + om * VEC, PO + om * 132, warp - 5, 2, err,
+                                   plan.poll_ns, plan.jitter, ahead);
+            if (trw) s_wM[warp] += sp::gtimer() - s_tr[0];
+            ahead = band_counters_ahead<17>(fa, b, d + 4, NS, need, warp - 5, 2);
+          }
+        } else {
+          if (res && d + 1 <= dlast)
+            sp::band_pre<M, BW>(f, ctx, b, d + 1, O + o1 * VEC, PO + o1 * 132,
+                                smem + LY::PRE + ((d + 1) & 1) * sp::PRE_N * 32);
+          // band k-1's new cell of diagonal d (the next step's x-upstream halo)
+          if (k > 0 && d + 1 <= dlast) {
+            double* hv = (res ? O + o0 * VEC : smem + (LY::V_V + (d & 1)) * VEC) + 32;
+            double* hp = (res ? PO + o0 * 132 : smem + LY::PV + (d & 1) * 132) + 128;
+            const int cl = b.cell(-1, d);
+            if (cl >= 0) {
+              const unsigned need = res ? rneed : ep + (unsigned)s + 1u;
+              sp::sched_jitter(plan.jitter, (unsigned)d);
+              if (c == 0 && need) poll_acquire(fa.vptr(cl), need, cl, b.nx, err, plan.poll_ns);
+              if (trw) s_wM[warp] += sp::gtimer() - s_tr[0];
+              __syncwarp();
+              const double r0 = c < N ? __ldcg(fa.cptr(cl, NP) + c) : 0.0;
+              const double r1 = c + 32 < N ? __ldcg(fa.cptr(cl, NP) + c + 32) : 0.0;
+              const double pr = c < 4 ? __ldcg(fa.pptr(cl) + c) : 0.0;
+              if (c < N) hv[c * SPV] = r0;
+              if (c + 32 < N) hv[(c + 32) * SPV] = r1;
+              if (c < 4) hp[c] = pr;
+            } else {
+              if (c < N) hv[c * SPV] = 0.0;
+              if (c + 32 < N) hv[(c + 32) * SPV] = 0.0;
+              if (c < 4) hp[c] = 0.0;
+            }
+          }
+        }
         if (warp == 2 && c == 0) s_stop = stop_now;
-      } else if (warp == 7) {
-        if (res && d + 1 <= dlast)
-          sp::band_pre<M, BW>(f, ctx, b, d + 1, O + o1 * VEC, PO + o1 * 132,
-                              smem + LY::PRE + ((d + 1) & 1) * sp::PRE_N * 32);
-        // band k-1's new cell of diagonal d (the next step's x-upstream halo)
-        if (k > 0 && d + 1 <= dlast)
-          sp::band_load<M, 1>(fa, b, d, -1, 1, res ? rneed : ep + (unsigned)s + 1u,
-                              (res ? O + o0 * VEC : smem + (LY::V_V + (d & 1)) * VEC) + 32, SPV,
-                              (res ? PO + o0 * 132 : smem + LY::PV + (d & 1) * 132) + 128, 0, 1, err, plan.poll_ns,
-                              plan.jitter, false);
       }
+      if (trw) s_wC[warp] += sp::gtimer() - s_tr[0];
       __syncthreads();
+      if (tr) s_tr[5] += sp::gtimer() - s_tr[0];
       if (s_stop) return;
     }
     if (!res) rb_writeback<M>(f, b, dlast, smem + (LY::V_V + (dlast & 1)) * VEC, smem + LY::PV + (dlast & 1) * 132,
-                              s_ok, 4 * warp, 4);
+                              s_ok[dlast & 1], 4 * warp, 4);
     __syncthreads();
     if (!res && warp == 1) {
+      const int cp_ = dlast > dfirst ? b.cell(c, dlast - 1) : -1;  // (written back during step dlast)
+      if (cp_ >= 0) st_release_s(fa.vptr(cp_), ep + (unsigned)s + 1u, false);
       const int cl = b.cell(c, dlast);
       if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, false);
     }
@@ -603,6 +737,20 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
       o[1] = sp::gtimer();
       o[2] = (unsigned long long)(dlast - dfirst + 1) | ((unsigned long long)s << 20) | ((unsigned long long)k << 28);
       for (int t = 3; t < 32; ++t) o[t] = 0;
+      o[3] = s_tr[1];
+      o[4] = s_tr[2];
+      o[12] = s_tr[3];
+      o[5] = s_tr[4];
+      o[7] = s_tr[5];
+      for (int w = 0; w < 8; ++w) {
+        o[16 + w] = s_wA[w];
+        o[24 + w] = s_wC[w];
+        if (w >= 2 && w != 6) o[6 + w] = s_wM[w];  // [8..13]: mid-role stamps of warps 2..7 (warp 6 in [14])
+      }
+      o[10] = 0;  // (marks the k8 stamp set; warp 4's mid-role stamp is not kept)
+      o[12] = s_tr[3];
+      o[14] = s_wM[6];
+
     }
   }
 }

@@ -33,6 +33,22 @@ sk = [(int(v >> 20) & 0xff, int(v >> 28)) for v in buf[:got, 2]]
 t0 = t[:, 0].min()
 S = np.sum(steps)
 print(f"tasks {got}  span {(t[:, 1].max() - t0) / 1e3:.1f} us")
+if np.sum(t[:, 10]) == 0:  # register-resident kernel (k8_band): its own stamp set
+    m = lambda q: np.sum(t[:, q]) / S / 1e3
+    print("k8_band per-step means, us from step start: write-back %.2f  faces(barrier A) %.2f  assembled(barrier B) %.2f"
+          "  updated(warp 0) %.2f  end(barrier C) %.2f;  loop time/step %.2f"
+          % (m(3), m(4), m(12), m(5), m(7), np.sum(t[:, 1] - t[:, 0]) / S / 1e3))
+    print("per-warp arrival at barrier A:", " ".join("%.2f" % m(16 + w) for w in range(8)))
+    print("per-warp arrival at barrier C:", " ".join("%.2f" % m(24 + w) for w in range(8)))
+    print("mid-role stamps, warps 2..7 (2-4 after the release, 5-6 after the cp.async issue, 7 after the halo poll):",
+          " ".join("%.2f" % m(q) for q in (8, 9, 11, 14, 13)), "(warps 2, 3, 5, 6, 7)")
+    print(" task  s   k  loop(us)  end(us)  steps  us/step")
+    for r in (list(range(0, min(4, got))) + list(range(nb - 2, nb + 2)) + list(range(got - 3, got))):
+        if 0 <= r < got:
+            s_, k_ = sk[r]
+            print(f"{r:5d} {s_:2d} {k_:3d} {(t[r,0]-t0)/1e3:8.1f} {(t[r,1]-t0)/1e3:8.1f} "
+                  f"{int(steps[r]):6d} {(t[r,1]-t[r,0])/steps[r]/1e3:8.2f}")
+    sys.exit(0)
 print("per-step means, us from step start: copies %.2f  faces %.2f  update %.2f  prefetch %.2f  end %.2f;"
       "  loop time/step %.2f" % tuple([np.sum(t[:, q]) / S / 1e3 for q in (3, 4, 5, 6, 7)]
                                       + [np.sum(t[:, 1] - t[:, 0]) / S / 1e3]))
