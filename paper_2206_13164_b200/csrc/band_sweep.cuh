@@ -98,6 +98,8 @@ struct BandPlan {
   // band's first column is the NEW state, that block ran earlier)
   const short* korder;
   const unsigned char* bflags;
+  // the second-order / rhs register kernel (reg_band2.cuh): spatial order 1 | 2, FAS right-hand side
+  int order, has_rhs;
 };
 
 template <int M>

@@ -427,6 +427,14 @@ bool band_sweep_enabled();
 // sweeps / residuals of M <= 5 (momg_set_band_kernel: 1 default, 0 k5_band)
 bool rb_enabled();
 
+// rb::k9_band (reg_band2.cuh, own translation units rb2_m<M>.cu)
+void rb2_launch_m3(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const sp::BandPlan& plan,
+                   cudaStream_t st);
+void rb2_launch_m4(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const sp::BandPlan& plan,
+                   cudaStream_t st);
+void rb2_launch_m5(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const sp::BandPlan& plan,
+                   cudaStream_t st);
+
 // launch of rb::k8_band (grid: one CTA per SM, at most one per task)
 template <int M, bool RES>
 void rb_launch(const DevField& f, const DevCtx& ctx, const sp::BandPlan& bp, const DevField& out) {
@@ -644,6 +652,28 @@ struct Launch {
             int nb = tc_sweep_blocks((const void*)sp::k5_band<M, 32>, sp::BandLayout<M>::bytes, sp::THREADS);
             if (nb > bp.nsweeps * bp.nbands) nb = bp.nsweeps * bp.nbands;
             sp::k5_band<M, 32><<<nb, sp::THREADS, sp::BandLayout<M>::bytes, momg_rt::stream()>>>(fd, c, err, bp, fd);
+            momg_rt::count_launch(1);
+            return;
+          }
+          if (rb_enabled() && ctx.threads <= 1) {
+            // second order and/or an FAS rhs, exact order: the register-resident kernel
+            sp::BandPlan bp{};
+            band_scratch(f, &bp.ver, &bp.next);
+            bp.nsweeps = 4 * iters;
+            bp.nbands = (f->nx + 31) / 32;
+            bp.nk = bp.nbands;
+            bp.dirbits = 0;
+            for (int s = 0; s < 16; ++s) {
+              bp.dirs[s] = order[s & 3];
+              bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
+            }
+            bp.order = ctx.order;
+            bp.has_rhs = rhs != nullptr;
+            bp.jitter = sched_jitter_seed();
+            bp.trace = trace_buffer(&bp.trace_cap);
+            if constexpr (M == 3) rb2_launch_m3(fd, rd, c, err, bp, momg_rt::stream());
+            else if constexpr (M == 4) rb2_launch_m4(fd, rd, c, err, bp, momg_rt::stream());
+            else rb2_launch_m5(fd, rd, c, err, bp, momg_rt::stream());
             momg_rt::count_launch(1);
             return;
           }

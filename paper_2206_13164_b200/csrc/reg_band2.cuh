@@ -4,8 +4,8 @@
 // = one sweep x one band of 32 rotated columns walked diagonal by diagonal,
 // 8 warps = 4 faces x {cell side, neighbour side}, one THREAD per face side
 // with the whole moment vector in registers, assembly split over the warps,
-// update in registers on warp 0, old states copied in two steps ahead with
-// cp.async, counters read one step ahead), what changes is the stencil:
+// update in registers on warp 0, old states copied in with cp.async under the
+// update, counters read one step ahead), what changes is the stencil:
 //
 //  * second-order face states (spatial.cpp:34-80) reach two cells along each
 //    axis: a side's state is  w = c + (off / h) (hi - lo)  of three on-chip
@@ -19,13 +19,17 @@
 //  * coarse levels subtract the projected right-hand side
 //    (single_level.cpp:64-70): an otherwise idle warp projects the rhs of
 //    diagonal d+1 into its cells' bases one step ahead (vector R);
-//  * the two sides of a face are summed in the face's F vector (a 64-thread
-//    named barrier per face) so that 4 + 1 + 4 + 2 = 11 vectors of 34 slots
-//    fit shared memory.
+//  * 14 vectors of 34 slots fit shared memory: old ring 4, new ring 2, the
+//    cell sides' F[4], R, and three vectors X[3] for the neighbour sides of
+//    faces 0..2 -- face 3's neighbour side uses the old-ring slot that is
+//    dead until phase (C) starts the next copy into it.
 //
 // Compiled in its own translation units (rb2_m<M>.cu) with SPV = 35.
 #pragma once
 
+#include "momg_cell.cuh"
+#include "sweep_persistent.cuh"
+#include "kernels_v3.cuh"
 #include "reg_band.cuh"
 
 namespace momg_gpu {
@@ -38,16 +42,15 @@ struct R2Layout {
   static constexpr int N = Gen<M>::N;
   static constexpr int VEC = N * SPV;
   // vectors: O[4] old ring (slot = column), V[2] new ring (slot = column + 2),
-  // F[4] faces (F[0] doubles as the assembled delta D), R projected rhs
-  static constexpr int V_O = 0, V_V = 4, V_F = 6, V_R = 10, NV = 11;
+  // F[4] cell sides of the faces (F[0] doubles as the assembled delta D), R
+  // projected rhs, X[3] neighbour sides of faces 0..2
+  static constexpr int V_O = 0, V_V = 4, V_F = 6, V_R = 10, V_X = 11, NV = 14;
   static constexpr int PS = 34 * 4;         // params of one vector
   static constexpr int PO = NV * VEC;       // [4][34][4]
   static constexpr int PV = PO + 4 * PS;    // [2][34][4]
   static constexpr int PRE = PV + 2 * PS;   // [2][PRE_N][32]
   static constexpr size_t bytes = (size_t)(PRE + 2 * sp::PRE_N * 32) * sizeof(double);
 };
-
-__device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 // the seven coefficients the wave-speed bounds read (rho, the three first
 // moments, the three 2 e_d) of  c + a (hi - lo)
@@ -75,7 +78,7 @@ __device__ __forceinline__ double rep_theta7(const double (&s)[7], const P4& p) 
 }
 
 struct Asm2Args {
-  const double *S, *Fxh, *Fxl, *Fyh, *Fyl, *R;
+  const double *S, *Fxh0, *Fxh1, *Fxl0, *Fxl1, *Fyh0, *Fyh1, *Fyl0, *Fyl1, *R;
   double nu, shw, idx, idy, s0;
   bool shk, rhs;
   const double* qv;
@@ -89,8 +92,8 @@ __device__ __forceinline__ void assemble2_one(const Asm2Args& a) {
     if (a.shk) eq = a.shw * a.qv[sd];
   }
   constexpr int o = K * SPV;
-  const double fx = a.Fxh[o] - a.Fxl[o];
-  const double fy = a.Fyh[o] - a.Fyl[o];
+  const double fx = (a.Fxh0[o] + a.Fxh1[o]) - (a.Fxl0[o] + a.Fxl1[o]);
+  const double fy = (a.Fyh0[o] + a.Fyh1[o]) - (a.Fyl0[o] + a.Fyl1[o]);
   double r = a.nu * (eq - a.S[o]);
   r -= fx * a.idx;
   r -= fy * a.idy;
@@ -286,12 +289,17 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
         const int i = b.i_up ? ir : f.nx - 1 - ir, j = b.j_up ? jr : f.ny - 1 - jr;
         const int pos = axis == 0 ? i : j;
         const bool has_nb = valid && (high ? pos + 1 < nax : pos >= 1);
-        double* F = smem + (LY::V_F + fw) * VEC + c;
+        // this side's vector: scratch for the projected state, then its flux in the cell basis
+        double* F = (side == 0 ? smem + (LY::V_F + fw) * VEC
+                               : (fw < 3 ? smem + (LY::V_X + fw) * VEC : O + ((d + 3) & 3) * VEC)) + c;
         int fail = W_NONE;
         int branch = sp::B_NONE;
         P4 to{}, from{};
         double rs = 1.0;
-        double v[N];
+        // this side's state: Mv, or Mv + a_me (Mhi - Mlo) when reconstructed (rme_ok)
+        const double *Mv = Sc, *Mhi = Sc, *Mlo = Sc;
+        double a_me = 0.0;
+        bool rme_ok = false;
         const bool my_left = side == 0 ? high : !high;  // left = lower-index cell of the face
         if (valid && !has_nb) {
           if (side == 0) {  // wall closure on the cell's own (unreconstructed) state, spatial.cpp:105-111
@@ -307,7 +315,6 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
               branch = sp::B_WALL;
               rs = sqrt(to.v[3]);
               from = cp;
-              vload<M>(Sc, v);
             }
           }
         } else if (valid) {
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
           const int rme = side == 0 ? 0 : rn, rot = side == 0 ? rn : 0;
           const int pme = side == 0 ? pos : (high ? pos + 1 : pos - 1);
           const int pot = side == 0 ? (high ? pos + 1 : pos - 1) : pos;
-          const double *Mv, *Mp, *Ov, *Op;
+          const double *Mp, *Ov, *Op;
           at(rme, &Mv, &Mp);
           at(rot, &Ov, &Op);
           const P4 mp0 = pload(Mp), op0 = pload(Op);
@@ -327,9 +334,9 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
           // me is the face's lower cell iff my_left: its face is its high face (off = +dx/2)
           const bool rec_me = o2 && pme > 0 && pme < nax - 1;
           const bool rec_ot = o2 && pot > 0 && pot < nax - 1;
-          double a_me = 0.0, a_ot = 0.0;
-          bool rme_ok = false, rot_ok = false;
-          const double *Mhi = nullptr, *Mlo = nullptr, *Ohi = nullptr, *Olo = nullptr;
+          double a_ot = 0.0;
+          bool rot_ok = false;
+          const double *Ohi = nullptr, *Olo = nullptr;
           const int up1 = a_up ? 1 : -1;  // rotated offset of original +1
           if (rec_me) {
             const double *hp, *lp_;
@@ -361,47 +368,55 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
               a_ot = off * ih;
             }
           }
-          // my state in registers
+          // wave-speed bounds (flux.cpp:79-84) from both face states, through
+          // the seven coefficients they read (before this side's vector is
+          // loaded: fewer live registers)
+          {
+            double m7[7], o7[7];
+            recon7(Mv, rme_ok ? Mhi : Mv, rme_ok ? Mlo : Mv, a_me, rme_ok, m7);
+            recon7(Ov, rot_ok ? Ohi : Ov, rot_ok ? Olo : Ov, a_ot, rot_ok, o7);
+            const P4 lp = my_left ? mp : opp;
+            const P4 rp = my_left ? opp : mp;
+            double l7[7], r7[7];
+#pragma unroll
+            for (int t = 0; t < 7; ++t) {
+              l7[t] = my_left ? m7[t] : o7[t];
+              r7[t] = my_left ? o7[t] : m7[t];
+            }
+            const double ul = (axis == 0 ? lp.v[0] : lp.v[1]) + (axis == 0 ? l7[1] : l7[2]) * (1.0 / l7[0]);
+            const double ur = (axis == 0 ? rp.v[0] : rp.v[1]) + (axis == 0 ? r7[1] : r7[2]) * (1.0 / r7[0]);
+            const double cl = ctx.c_bound * sqrt(rep_theta7(l7, lp));
+            const double cr = ctx.c_bound * sqrt(rep_theta7(r7, rp));
+            const double lminus = tc::smin(ul - cl, ur - cr);
+            const double lplus = tc::smax(ul + cl, ur + cr);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) to.v[q] = 0.5 * (lp.v[q] + rp.v[q]);
+            if (!(to.v[3] > 0.0)) {
+              fail = W_PROJ_SPREAD;
+            } else {
+              branch = lminus >= 0.0 ? sp::B_FULL_L : (lplus <= 0.0 ? sp::B_FULL_R : sp::B_HALF);
+              rs = sqrt(to.v[3]);
+              if ((branch == sp::B_FULL_L && !my_left) || (branch == sp::B_FULL_R && my_left)) branch = sp::B_NONE;
+              from = mp;
+            }
+          }
+        }
+        double v[N];
+        if (branch == sp::B_NONE) {
+#pragma unroll
+          for (int kk = 0; kk < N; ++kk) v[kk] = 0.0;
+        } else {
+          const bool full = branch == sp::B_FULL_L || branch == sp::B_FULL_R;
+          const bool wall = branch == sp::B_WALL;
+          // this side's state in registers
           if (rme_ok) {
 #pragma unroll
-            for (int kk = 0; kk < N; ++kk)
-              v[kk] = fma(a_me, Mhi[kk * SPV] - Mlo[kk * SPV], Mv[kk * SPV]);
+            for (int kk = 0; kk < N; ++kk) v[kk] = fma(a_me, Mhi[kk * SPV] - Mlo[kk * SPV], Mv[kk * SPV]);
           } else {
             vload<M>(Mv, v);
           }
-          // wave-speed bounds (flux.cpp:79-84) from both face states
-          double o7[7];
-          recon7(Ov, rot_ok ? Ohi : Ov, rot_ok ? Olo : Ov, a_ot, rot_ok, o7);
-          const double m7[7] = {v[0], v[1], v[2], v[3], v[4], v[7], v[9]};
-          const P4& lp = my_left ? mp : opp;
-          const P4& rp = my_left ? opp : mp;
-          const double(&l7)[7] = my_left ? m7 : o7;
-          const double(&r7)[7] = my_left ? o7 : m7;
-          const double ul = (axis == 0 ? lp.v[0] : lp.v[1]) + l7[1 + axis] * (1.0 / l7[0]);
-          const double ur = (axis == 0 ? rp.v[0] : rp.v[1]) + r7[1 + axis] * (1.0 / r7[0]);
-          const double cl = ctx.c_bound * sqrt(rep_theta7(l7, lp));
-          const double cr = ctx.c_bound * sqrt(rep_theta7(r7, rp));
-          const double lminus = tc::smin(ul - cl, ur - cr);
-          const double lplus = tc::smax(ul + cl, ur + cr);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) to.v[q] = 0.5 * (lp.v[q] + rp.v[q]);
-          if (!(to.v[3] > 0.0)) {
-            fail = W_PROJ_SPREAD;
-          } else {
-            branch = lminus >= 0.0 ? sp::B_FULL_L : (lplus <= 0.0 ? sp::B_FULL_R : sp::B_HALF);
-            rs = sqrt(to.v[3]);
-            if ((branch == sp::B_FULL_L && !my_left) || (branch == sp::B_FULL_R && my_left)) branch = sp::B_NONE;
-            from = mp;
-          }
-        }
-        if (branch != sp::B_NONE) {
-          const bool full = branch == sp::B_FULL_L || branch == sp::B_FULL_R;
-          const bool wall = branch == sp::B_WALL;
           xf::project_row<M>(v, from, to);
-          // through F once (this side's slot until the pair barrier): the
-          // flux reads it back pencil by pencil
-          double* T = side == 0 ? F : R + c;
-          (void)T;
+          // through F once: the flux reads it back pencil by pencil
           vstore<M>(F, v);
           asm volatile("" ::: "memory");
           if (full) {
@@ -427,25 +442,10 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
               v[0] = 0.0;
             }
           }
-          xf::project_row<M>(v, to, cp);
+          xf::project_row<M>(v, to, pload(Sp));
         }
+        vstore<M>(F, v);
         if (fail && valid && side == 0) tc::raise(err, tc::code_for(fail), fail, i, j, 0.0);
-        // the two sides of the face summed in F: side 0 stores, side 1 adds
-        (void)branch;
-        if (side == 0) {
-          if (branch == sp::B_NONE) {
-#pragma unroll
-            for (int kk = 0; kk < N; ++kk) v[kk] = 0.0;
-          }
-          vstore<M>(F, v);
-          pair_bar(1 + fw);
-        } else {
-          pair_bar(1 + fw);
-          if (branch != sp::B_NONE) {
-#pragma unroll
-            for (int kk = 0; kk < N; ++kk) F[kk * SPV] += v[kk];
-          }
-        }
       }
       __syncthreads();
       if (tr) s_tr[2] += sp::gtimer() - s_tr[0];
@@ -456,11 +456,18 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
         const double* Fb = smem + LY::V_F * VEC + c;
         const double qv[3] = {pre[sp::PRE_Q0 * 32], pre[sp::PRE_Q0 * 32 + 32], pre[sp::PRE_Q0 * 32 + 64]};
         const double* S = O + (d & 3) * VEC + c;
+        const double* Xb = smem + LY::V_X * VEC + c;
+        const double* X3 = O + ((d + 3) & 3) * VEC + c;  // face 3's neighbour side
+        const int fxl = 1 - fxh, fyl = 5 - fyh;
         const Asm2Args a{S,
                          Fb + fxh * VEC,
-                         Fb + (1 - fxh) * VEC,
+                         Xb + fxh * VEC,
+                         Fb + fxl * VEC,
+                         Xb + fxl * VEC,
                          Fb + fyh * VEC,
-                         Fb + (5 - fyh) * VEC,
+                         fyh < 3 ? Xb + fyh * VEC : X3,
+                         Fb + fyl * VEC,
+                         fyl < 3 ? Xb + fyl * VEC : X3,
                          R + c,
                          pre[sp::PRE_NU * 32],
                          ctx.shakhov_w,
@@ -542,12 +549,14 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
           __syncwarp();
         }
       } else if (warp <= 6) {
-        cp_async_wait();
-        if (d + 3 <= dlast + 2) {  // old(d+3) is read up to step dlast (as old(d'+2), d' = d+1)
+        // old(d+3) is read from the next step on (as old(d'+2)): copied in
+        // during this phase, under the update
+        if (d + 1 <= dlast) {
           band_load_async<M, 17>(fa, b, d + 3, NS, nold, O + ((d + 3) & 3) * VEC, PO + ((d + 3) & 3) * PS, warp - 5, 2,
                                  err, plan.poll_ns, plan.jitter, ahead);
           ahead = band_counters_ahead<17>(fa, b, d + 4, NS, nold, warp - 5, 2);
         }
+        cp_async_wait();
       } else {
         // band k-1's columns -1 and -2 of diagonal d (slots 1, 0 of new(d))
         if (k > 0 && d + 1 <= dlast) {
