@@ -1,6 +1,6 @@
 """Per-task timeline of the band-persistent sweep (debug trace).
 
-usage: python tools/trace_band.py [n] [M]
+usage: python tools/trace_band.py [n] [M] [space order]
 """
 import ctypes as C
 import os
@@ -14,8 +14,9 @@ from paper_2206_13164_b200.synthetic import c5_field  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+SO = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 g = momg.Grid2D.uniform(n, n)
-ctx = momg.cavity_context(M, 1, knudsen=0.1, lid=0.0)
+ctx = momg.cavity_context(M, SO, knudsen=0.1, lid=0.0)
 c, p = c5_field(n, n, M, seed=1)
 f = momg.CellField.from_host(g, M, c, p)
 momg.fast_sweep_step(f, None, ctx)
