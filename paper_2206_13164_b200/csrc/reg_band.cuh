@@ -358,9 +358,16 @@ __device__ __forceinline__ void band_load_async(const Addr& fld, const Geo& b, i
         else vec[kk * SPV + slot] = 0.0;
       }
     }
-    if (lane < 4) {
-      if (cl >= 0) cp_async8(prm + slot * 4 + lane, fld.pptr(cl) + lane);
-      else prm[slot * 4 + lane] = 0.0;
+  }
+  // the slots' parameters, eight slots per instruction (4 lanes each)
+#pragma unroll
+  for (int r = 0; r < (MAXS + 7) / 8; ++r) {
+    const int t = 8 * r + (lane >> 2);
+    const int slot = wi + t * nw;
+    const int cl = __shfl_sync(0xffffffffu, my_cell, t < MAXS ? t : 0);
+    if (t < MAXS && slot < ns) {
+      if (cl >= 0) cp_async8(prm + slot * 4 + (lane & 3), fld.pptr(cl) + (lane & 3));
+      else prm[slot * 4 + (lane & 3)] = 0.0;
     }
   }
 }
@@ -386,10 +393,13 @@ __device__ __forceinline__ void rb_writeback(const DevField& f, const Geo& b, in
                                              const double* PV, const int* ok, int c0, int nc) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3, H = (N + 31) / 32;
   const int lane = threadIdx.x & 31;
-#pragma unroll 1
+  // the cells' indices by the lanes up front (no dependent chain per cell)
+  int mine = -1;
+  if (lane < nc && ok[c0 + lane]) mine = b.cell(c0 + lane, dd);
+#pragma unroll 2
   for (int t = 0; t < nc; ++t) {
     const int cc = c0 + t;
-    const int cl = ok[cc] ? b.cell(cc, dd) : -1;
+    const int cl = __shfl_sync(0xffffffffu, mine, t);
     if (cl < 0) continue;
     double* dst = f.c + (size_t)cl * NP;
     double r[H];
@@ -522,7 +532,7 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
     // F pointers of the assembly: [x high side0, side1, x low ..., y high ..., y low ...]
     const bool xu_high = !b.i_up, yu_high = !b.j_up;
     const int fxh = xu_high ? 0 : 1, fyh = yu_high ? 2 : 3;
-    unsigned ahead = 0u;  // warps 5, 6: the counters of the next diagonal to copy, read one step ahead
+    unsigned ahead = 0u;  // warps 2, 5, 6: the counters of the next diagonal to copy, read one step ahead
     for (int d = dfirst; d <= dlast; ++d) {
       // old(d), old(d+1); om: old(d-1) (residual tasks) until phase (C) starts the copy of old(d+3) into it
       const int o0 = d & 3, o1 = (d + 1) & 3, om = (d + 3) & 3;
@@ -660,34 +670,36 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
       } else {  // warps 2..7
         const int stop_now = warp == 2 && c == 0 ? sp::band_stop(err) : 0;
         // every role below is one or two dependent memory round trips, shorter than warp 0's update
-        if (warp <= 4) {
-          // publication of step d-2 (its stores were issued a step ago: the
-          // release has nothing to wait for), then the write-back of step d-1
-          // (final since the last CTA barrier); a contiguous third of the 32
-          // cells per warp
-          if (!res && d > dfirst) {
-            const int wq = warp - 2, c0 = 11 * wq, nc = wq < 2 ? 11 : 10;
+        if (warp == 2) {
+          // publication of step d-2: its stores were issued a step ago by
+          // warps 3, 4 (ordered by that step's CTA barrier), so the one
+          // release of the step has nothing to wait for
+          if (!res && d - 2 >= dfirst) {
             sp::sched_jitter(plan.jitter, (unsigned)d);
-            if (d - 2 >= dfirst && c < nc) {
-              const int cl = b.cell(c0 + c, d - 2);
-              if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, false);
-            }
+            const int cl = b.cell(c, d - 2);
+            if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, false);
+          }
+        } else if (warp <= 4) {
+          // write-back of step d-1 (final since the last CTA barrier), 16 cells per warp
+          if (!res && d > dfirst) {
             if (trw) s_wM[warp] += sp::gtimer() - s_tr[0];
             rb_writeback<M>(f, b, d - 1, smem + (LY::V_V + ((d - 1) & 1)) * VEC, smem + LY::PV + ((d - 1) & 1) * 132,
-                            s_ok[(d - 1) & 1], c0, nc);
-            __syncwarp();
+                            s_ok[(d - 1) & 1], 16 * (warp - 3), 16);
           }
-        } else if (warp <= 6) {
-          // old(d+2), issued one step ago, has landed; start the copy of old(d+3)
+        }
+        if (warp == 2 || warp == 5 || warp == 6) {
+          // old(d+2), issued one step ago, has landed; start the copy of
+          // old(d+3), a third of the 33 slots per warp
+          const int wi = warp == 2 ? 2 : warp - 5;
           cp_async_wait();
           if (d + 2 <= dlast) {
             const unsigned need = res ? rneed : ep + (unsigned)s;
-            band_load_async<M, 17>(fa, b, d + 3, NS, need, O + om * VEC, PO + om * 132, warp - 5, 2, err,
-                                   plan.poll_ns, plan.jitter, ahead);
+            band_load_async<M, 11>(fa, b, d + 3, NS, need, O + om * VEC, PO + om * 132, wi, 3, err, plan.poll_ns,
+                                   plan.jitter, ahead);
             if (trw) s_wM[warp] += sp::gtimer() - s_tr[0];
-            ahead = band_counters_ahead<17>(fa, b, d + 4, NS, need, warp - 5, 2);
+            ahead = band_counters_ahead<11>(fa, b, d + 4, NS, need, wi, 3);
           }
-        } else {
+        } else if (warp == 7) {
           if (res && d + 1 <= dlast)
             sp::band_pre<M, BW>(f, ctx, b, d + 1, O + o1 * VEC, PO + o1 * 132,
                                 smem + LY::PRE + ((d + 1) & 1) * sp::PRE_N * 32);

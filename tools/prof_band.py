@@ -12,8 +12,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--nx", type=int, default=32)
 ap.add_argument("--ny", type=int, default=1024)
 ap.add_argument("--M", type=int, default=5)
+ap.add_argument("--order", type=int, default=1)
 a = ap.parse_args()
-ctx = momg.cavity_context(a.M, 1, knudsen=0.1, lid=0.0)
+ctx = momg.cavity_context(a.M, a.order, knudsen=0.1, lid=0.0)
 g = momg.Grid2D.uniform(a.nx, a.ny)
 c, p = c5_field(a.nx, a.ny, a.M, seed=1)
 f = momg.CellField.from_host(g, a.M, c, p)

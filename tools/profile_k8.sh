@@ -21,6 +21,19 @@ ncu --set full --clock-control none --import-source on -k regex:"k8_band" -c 1 \
     -o /tmp/band_k8 -f python tools/prof_band.py > gpurun_out/ncu_band_k8.log 2>&1
 python tools/ncu_summary.py /tmp/band_k8.ncu-rep k8_band 40 > gpurun_out/r2_ncu_k8_summary.txt 2>&1
 python tools/ncu_lines.py /tmp/band_k8.ncu-rep 70 > gpurun_out/r2_ncu_k8_lines.txt 2>&1
+# 3b) the same for the second-order kernel (k9_band), and the launch list of C2 NMG V-cycles
+python tools/prof_band.py --order 2 > gpurun_out/plain_band_k9.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k9_band" -c 1 \
+    -o /tmp/band_k9 -f python tools/prof_band.py --order 2 > gpurun_out/ncu_band_k9.log 2>&1
+python tools/ncu_summary.py /tmp/band_k9.ncu-rep k9_band 40 > gpurun_out/r2_ncu_k9_summary.txt 2>&1
+python tools/ncu_lines.py /tmp/band_k9.ncu-rep 50 > gpurun_out/r2_ncu_k9_lines.txt 2>&1
+python tools/prof_nmg.py > gpurun_out/plain_nmg_k9.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_k9_nmg_launches.csv \
+    python tools/prof_nmg.py > gpurun_out/ncu_nmg_k9.log 2>&1
+python tools/launch_summary.py gpurun_out/r2_k9_nmg_launches.csv \
+  "# ncu launch list, C2 NMG V-cycles (tools/prof_nmg.py; k9_band = second-order / rhs register-resident band sweep)" \
+  > gpurun_out/r2_k9_nmg_launches_summary.txt
+python tools/trace_band.py 128 5 2 > gpurun_out/r2_k9_trace_128.txt 2>&1
 # 4) band step trace at 2048^2 (per-phase %globaltimer stamps, not timed)
 python tools/trace_band.py 2048 > gpurun_out/r2_k8_trace_2048.txt 2>&1
 echo profile done

@@ -43,6 +43,13 @@ if np.sum(t[:, 10]) == 0:  # register-resident kernel (k8_band): its own stamp s
     print("per-warp arrival at barrier C:", " ".join("%.2f" % m(24 + w) for w in range(8)))
     print("mid-role stamps, warps 2..7 (2-4 after the release, 5-6 after the cp.async issue, 7 after the halo poll):",
           " ".join("%.2f" % m(q) for q in (8, 9, 11, 14, 13)), "(warps 2, 3, 5, 6, 7)")
+    ups = (t[:, 1] - t[:, 0]) / np.maximum(steps, 1) / 1e3
+    for sw in range(4):
+        rows_ = [r for r in range(got) if sk[r][0] == sw]
+        if rows_:
+            q = np.array_split(np.array(rows_), 4)
+            print(f"sweep {sw}: us/step by band quarter:", " ".join("%.2f" % ups[x].mean() for x in q if len(x)),
+                  "| start %.1f ms end %.1f ms" % ((t[rows_, 0].min() - t0) / 1e6, (t[rows_, 1].max() - t0) / 1e6))
     print(" task  s   k  loop(us)  end(us)  steps  us/step")
     for r in (list(range(0, min(4, got))) + list(range(nb - 2, nb + 2)) + list(range(got - 3, got))):
         if 0 <= r < got:
