@@ -371,6 +371,7 @@ def ours(a):
     nmg = None
     if not a.no_nmg and rank == 0:
         nmg = run_nmg_c2(momg)
+        nmg["other_configs"] = run_nmg_configs(momg)
 
     # ---- roofline of the dominant kernel (persistent FS sweep)
     peak, peak_src = fp64_peak()
@@ -537,6 +538,40 @@ def run_nmg_c2(momg):
     out["blocked_threads8"] = {"seconds": time.perf_counter() - t, "converged": ok8, "iterations": rep8.iterations,
                                "note": "SolveContext.threads = 8 (the reference's blocked-parallel FS realised "
                                        "deterministically, DESIGN.md sec. 5); not the exact order above"}
+    return out
+
+
+def run_nmg_configs(momg, cycles=3):
+    """V-cycle time of the other BASELINE NMG configs on the device (C3: 256^2,
+    M = 8, Shakhov, Kn 0.01, 5 levels; C4: 512^2, M = 6, heated bottom wall, 6
+    levels): `cycles` NMG cycles from the uniform Maxwellian start, timed
+    after one warm-up cycle.  Their full solves and parity against the oracle
+    are in tests/test_gpu_configs.py and profiles/r2_configs_device.json; here
+    only the per-cycle time and its FP64 fraction (FS flops, SURVEY.md §8(a):
+    28,191 flop per cell update at M = 6 order 2, 70,484 at M = 8)."""
+    import torch
+    peak, _ = fp64_peak()
+    out = {}
+    for name, (n, M, model, kn, pr, lid, bt, levels, fl) in {
+            "C3": (256, 8, momg.CollisionKind.shakhov, 0.01, 2.0 / 3.0, 0.1, 1.0, 5, 70484.0),
+            "C4": (512, 6, momg.CollisionKind.bgk, 0.1, 1.0, 0.0, 2.0, 6, 28191.0)}.items():
+        ctx = momg.cavity_context(M, 2, model, knudsen=kn, lid=lid, prandtl=pr, bottom_theta=bt)
+        f = momg.uniform_field(momg.Grid2D.uniform(n, n), M, 1.0, (0.0, 0.0, 0.0), 1.0)
+        momg.nmg_cycle(f, ctx, levels)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(cycles):
+            momg.nmg_cycle(f, ctx, levels)
+        momg.synchronize()
+        ms = 1e3 * (time.perf_counter() - t) / cycles
+        updates = sum(16 * (n >> l) ** 2 for l in range(levels))  # 4 FS iterations x 4 sweeps per level
+        achieved = updates * fl / (ms * 1e-3) / 1e12
+        out[name] = {"config": f"{n}x{n} M={M} order 2 NMG levels {levels}", "ms_per_vcycle": ms,
+                     "cell_updates_per_vcycle": updates,
+                     "kernel": "rb::k9_band<6,16> (register-resident, 16-column bands)" if M == 6 else "k_sweep_persistent (warp per cell)",
+                     "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                                  "frac": achieved / peak}}
+        del f
     return out
 
 

@@ -434,6 +434,8 @@ void rb2_launch_m4(const DevField& f, const DevField& rhs, const DevCtx& ctx, De
                    cudaStream_t st);
 void rb2_launch_m5(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const sp::BandPlan& plan,
                    cudaStream_t st);
+void rb2_launch_m6(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const sp::BandPlan& plan,
+                   cudaStream_t st);  // 16-column bands
 
 // launch of rb::k8_band (grid: one CTA per SM, at most one per task)
 template <int M, bool RES>
@@ -607,6 +609,31 @@ struct Launch {
         return;
       }
     } else {
+      if constexpr (M == 6) {
+        // the register-resident band kernel with 16-column bands (rb2_m6.cu):
+        // every exact-order BGK / Shakhov sweep of M = 6 (first or second
+        // order, with or without rhs), up to four FS iterations per launch
+        if (band_sweep_enabled() && rb_enabled() && ctx.collision != 1 && ctx.threads <= 1 && iters <= 4) {
+          sp::BandPlan bp{};
+          band_scratch(f, &bp.ver, &bp.next);
+          bp.nsweeps = 4 * iters;
+          bp.nbands = (f->nx + 15) / 16;
+          bp.nk = bp.nbands;
+          bp.dirbits = 0;
+          for (int s = 0; s < 16; ++s) {
+            bp.dirs[s] = order[s & 3];
+            bp.dirbits |= (unsigned)(order[s & 3] & 3) << (2 * s);
+          }
+          bp.order = ctx.order;
+          bp.has_rhs = rhs != nullptr;
+          bp.jitter = sched_jitter_seed();
+          bp.trace = trace_buffer(&bp.trace_cap);
+          const DevField fd = f->dev();
+          rb2_launch_m6(fd, rhs ? rhs->dev() : fd, ctx, momg_rt::err_dev(), bp, momg_rt::stream());
+          momg_rt::count_launch(1);
+          return;
+        }
+      }
       for (int it = 0; it < iters; ++it) sweep1(ctx, f, rhs, order, 1);
       return;
     }

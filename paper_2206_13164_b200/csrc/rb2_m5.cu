@@ -7,6 +7,6 @@
 namespace momg_gpu {
 void rb2_launch_m5(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const sp::BandPlan& plan,
                    cudaStream_t st) {
-  rb::rb2_launch_impl<5>(f, rhs, ctx, err, plan, st);
+  rb::rb2_launch_impl<5, 32>(f, rhs, ctx, err, plan, st);
 }
 }  // namespace momg_gpu

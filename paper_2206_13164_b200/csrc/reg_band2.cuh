@@ -35,19 +35,21 @@
 namespace momg_gpu {
 namespace rb {
 
-static_assert(SPV >= 34, "k9 vectors need 34 slots (compile with SPV = 35)");
 
-template <int M>
+// BW: columns per band task (32; 16 for M = 6, whose 84-coefficient vectors
+// would not fit shared memory at 32)
+template <int M, int BW>
 struct R2Layout {
+  static_assert(SPV >= BW + 2, "k9 vectors need BW + 2 slots");
   static constexpr int N = Gen<M>::N;
   static constexpr int VEC = N * SPV;
   // vectors: O[4] old ring (slot = column), V[2] new ring (slot = column + 2),
   // F[4] cell sides of the faces (F[0] doubles as the assembled delta D), R
   // projected rhs, X[3] neighbour sides of faces 0..2
   static constexpr int V_O = 0, V_V = 4, V_F = 6, V_R = 10, V_X = 11, NV = 14;
-  static constexpr int PS = 34 * 4;         // params of one vector
-  static constexpr int PO = NV * VEC;       // [4][34][4]
-  static constexpr int PV = PO + 4 * PS;    // [2][34][4]
+  static constexpr int PS = (BW + 2) * 4;   // params of one vector
+  static constexpr int PO = NV * VEC;       // [4][BW + 2][4]
+  static constexpr int PV = PO + 4 * PS;    // [2][BW + 2][4]
   static constexpr int PRE = PV + 2 * PS;   // [2][PRE_N][32]
   static constexpr size_t bytes = (size_t)(PRE + 2 * sp::PRE_N * 32) * sizeof(double);
 };
@@ -162,34 +164,38 @@ template <int M, class Addr>
 __device__ __forceinline__ void load_slot(const Addr& fa, int cl, double* vec, double* prm, int sl) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3;
   const int c = threadIdx.x & 31;
-  const double r0 = (cl >= 0 && c < N) ? __ldcg(fa.cptr(cl, NP) + c) : 0.0;
-  const double r1 = (cl >= 0 && c + 32 < N) ? __ldcg(fa.cptr(cl, NP) + c + 32) : 0.0;
+  constexpr int H = (N + 31) / 32;
+  double r[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) r[h] = (cl >= 0 && c + 32 * h < N) ? __ldcg(fa.cptr(cl, NP) + c + 32 * h) : 0.0;
   const double pr = (cl >= 0 && c < 4) ? __ldcg(fa.pptr(cl) + c) : 0.0;
-  if (c < N) vec[c * SPV + sl] = r0;
-  if (c + 32 < N) vec[(c + 32) * SPV + sl] = r1;
+#pragma unroll
+  for (int h = 0; h < H; ++h)
+    if (c + 32 * h < N) vec[(c + 32 * h) * SPV + sl] = r[h];
   if (c < 4) prm[sl * 4 + c] = pr;
 }
 
 // The rhs of the cells of diagonal dd projected into their (old) bases, into
 // R (slot = column); lane = cell, the record in registers (transfer.cuh).
-template <int M, class Geo>
+template <int M, int BW, class Geo>
 __device__ __forceinline__ void rhs_project(const DevField& rhs, const Geo& b, int dd, const double* PO, double* R) {
   constexpr int N = Gen<M>::N, NP = (N + 3) & ~3;
   const int c = threadIdx.x & 31;
-  const int cl = b.cell(c, dd);
+  const int cl = c < BW ? b.cell(c, dd) : -1;
   if (cl < 0) return;
   double v[N];
   xf::load_rec<M, false>(rhs.c + (size_t)cl * NP, v);
   const P4 from = tc::ldp<false>(rhs.p + (size_t)cl * 4);
   const P4 to = pload(PO + c * 4);
-  if (to.v[3] > 0.0) xf::project_row<M>(v, from, to);
+  if (to.v[3] > 0.0) xf::project_row<M, (M <= 5)>(v, from, to);
   vstore<M>(R + c, v);
 }
 
-template <int M>
+template <int M, int BW>
 __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevCtx ctx, DevErr* err, BandPlan plan) {
-  constexpr int BW = 32, NS = BW + 2;
-  using LY = R2Layout<M>;
+  constexpr int NS = BW + 2;
+  constexpr int AM = (NS + 1) / 2;  // slots per copying warp
+  using LY = R2Layout<M, BW>;
   constexpr int N = LY::N, VEC = LY::VEC, PS = LY::PS;
   extern __shared__ __align__(128) double smem[];
   __shared__ int s_task, s_stop;
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
     if (warp == 1)
       sp::band_pre<M, BW>(f, ctx, b, dfirst, O + (dfirst & 3) * VEC, PO + (dfirst & 3) * PS,
                           smem + LY::PRE + (dfirst & 1) * sp::PRE_N * 32);
-    if (warp == 2 && has_rhs) rhs_project<M>(rhsf, b, dfirst, PO + (dfirst & 3) * PS, R);
+    if (warp == 2 && has_rhs) rhs_project<M, BW>(rhsf, b, dfirst, PO + (dfirst & 3) * PS, R);
     __syncthreads();
     if (tr) t0 = sp::gtimer();
     // face of this warp: fw = warp >> 1 (0 x-upstream, 1 x-downstream, 2
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
     for (int d = dfirst; d <= dlast; ++d) {
       if (tr) s_tr[0] = sp::gtimer();
       const int jr = d - ir;
-      const bool valid = ir < f.nx && jr >= 0 && jr < f.ny;
+      const bool valid = c < BW && ir < f.nx && jr >= 0 && jr < f.ny;
       // ---- (A) faces: this warp's side of its face for the 32 cells
       {
         // the cell at rotated offset r along the axis: (c + r, d + r) for
@@ -415,9 +421,9 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
           } else {
             vload<M>(Mv, v);
           }
-          xf::project_row<M>(v, from, to);
+          xf::project_row<M, (M <= 5)>(v, from, to);
           // through F once: the flux reads it back pencil by pencil
-          vstore<M>(F, v);
+          if (BW == 32 || c < BW) vstore<M>(F, v);
           asm volatile("" ::: "memory");
           if (full) {
             if (axis == 0) Gen<M>::template full_flux0<SPV, 1>(F, v, to.v[0], to.v[3]);
@@ -427,8 +433,18 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
             double K[M + 1][M + 1];
             double kin0[M + 1];
             half_kernel_side<M>(un, rs, tc::half_base(un, rs), wall ? high : my_left, K, kin0);
-            if (axis == 0) Gen<M>::template half_sr0<SPV, 1>(F, v, K);
-            else Gen<M>::template half_sr1<SPV, 1>(F, v, K);
+            if constexpr (M <= 5) {
+              if (axis == 0) Gen<M>::template half_sr0<SPV, 1>(F, v, K);
+              else Gen<M>::template half_sr1<SPV, 1>(F, v, K);
+            } else {
+              // the (M+1)^2 table and the vector do not fit the registers
+              // together: the flux runs in place in shared memory (a pencil's
+              // inputs are read before its outputs are written)
+              if (axis == 0) Gen<M>::template half_one0<SPV>(F, K);
+              else Gen<M>::template half_one1<SPV>(F, K);
+              asm volatile("" ::: "memory");
+              vload<M>(F, v);
+            }
             if (wall) {  // density of the incoming wall Maxwellian (flux.cpp:119-129)
               const double in0 = kin0[0];
               const double wall_rho = in0 == 0.0 ? 0.0 : -v[0] / in0;
@@ -442,9 +458,9 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
               v[0] = 0.0;
             }
           }
-          xf::project_row<M>(v, to, pload(Sp));
+          xf::project_row<M, (M <= 5)>(v, to, pload(Sp));
         }
-        vstore<M>(F, v);
+        if (BW == 32 || c < BW) vstore<M>(F, v);
         if (fail && valid && side == 0) tc::raise(err, tc::code_for(fail), fail, i, j, 0.0);
       }
       __syncthreads();
@@ -503,7 +519,7 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
 #pragma unroll
             for (int kk = 0; kk < N; ++kk) v[kk] = S[kk * SPV] + h * D[kk * SPV];
             prm = cp;
-            const int st = xf::normalize_row<M>(v, prm, &bad);
+            const int st = xf::normalize_row<M, (M <= 5)>(v, prm, &bad);
             if (st == W_NONE) {
               good = true;
               break;
@@ -534,27 +550,27 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
                               smem + LY::PRE + ((d + 1) & 1) * sp::PRE_N * 32);
       } else if (warp == 2) {
         const int stop_now = c == 0 ? sp::band_stop(err) : 0;
-        if (has_rhs && d + 1 <= dlast) rhs_project<M>(rhsf, b, d + 1, PO + ((d + 1) & 3) * PS, R);
+        if (has_rhs && d + 1 <= dlast) rhs_project<M, BW>(rhsf, b, d + 1, PO + ((d + 1) & 3) * PS, R);
         if (c == 0) s_stop = stop_now;
       } else if (warp <= 4) {
         // publication of step d-2 (stored a step ago), write-back of step d-1
         if (d > dfirst) {
-          const int c0 = 16 * (warp - 3);
+          const int c0 = (BW / 2) * (warp - 3);
           sp::sched_jitter(plan.jitter, (unsigned)d);
-          if (d - 2 >= dfirst && c < 16) {
+          if (d - 2 >= dfirst && c < BW / 2) {
             const int cl = b.cell(c0 + c, d - 2);
             if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, false);
           }
-          rb2_writeback<M>(f, b, d - 1, V + ((d - 1) & 1) * VEC, PV + ((d - 1) & 1) * PS, s_ok[(d - 1) & 1], c0, 16);
+          rb2_writeback<M>(f, b, d - 1, V + ((d - 1) & 1) * VEC, PV + ((d - 1) & 1) * PS, s_ok[(d - 1) & 1], c0, BW / 2);
           __syncwarp();
         }
       } else if (warp <= 6) {
         // old(d+3) is read from the next step on (as old(d'+2)): copied in
         // during this phase, under the update
         if (d + 1 <= dlast) {
-          band_load_async<M, 17>(fa, b, d + 3, NS, nold, O + ((d + 3) & 3) * VEC, PO + ((d + 3) & 3) * PS, warp - 5, 2,
+          band_load_async<M, AM>(fa, b, d + 3, NS, nold, O + ((d + 3) & 3) * VEC, PO + ((d + 3) & 3) * PS, warp - 5, 2,
                                  err, plan.poll_ns, plan.jitter, ahead);
-          ahead = band_counters_ahead<17>(fa, b, d + 4, NS, nold, warp - 5, 2);
+          ahead = band_counters_ahead<AM>(fa, b, d + 4, NS, nold, warp - 5, 2);
         }
         cp_async_wait();
       } else {
@@ -573,12 +589,13 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
       if (tr) s_tr[5] += sp::gtimer() - s_tr[0];
       if (s_stop) return;
     }
-    rb2_writeback<M>(f, b, dlast, V + (dlast & 1) * VEC, PV + (dlast & 1) * PS, s_ok[dlast & 1], 4 * warp, 4);
+    rb2_writeback<M>(f, b, dlast, V + (dlast & 1) * VEC, PV + (dlast & 1) * PS, s_ok[dlast & 1], (BW / 8) * warp,
+                     BW / 8);
     __syncthreads();
     if (warp == 1) {
-      const int cp_ = dlast > dfirst ? b.cell(c, dlast - 1) : -1;  // (written back during step dlast)
+      const int cp_ = dlast > dfirst && c < BW ? b.cell(c, dlast - 1) : -1;  // (written back during step dlast)
       if (cp_ >= 0) st_release_s(fa.vptr(cp_), ep + (unsigned)s + 1u, false);
-      const int cl = b.cell(c, dlast);
+      const int cl = c < BW ? b.cell(c, dlast) : -1;
       if (cl >= 0) st_release_s(fa.vptr(cl), ep + (unsigned)s + 1u, false);
     }
     if (tr) {
@@ -595,19 +612,19 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
   }
 }
 
-template <int M>
+template <int M, int BW>
 void rb2_launch_impl(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const BandPlan& plan,
                      cudaStream_t st) {
   static int nsm = 0;
   if (!nsm) {
-    cudaFuncSetAttribute(k9_band<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R2Layout<M>::bytes);
+    cudaFuncSetAttribute(k9_band<M, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R2Layout<M, BW>::bytes);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   int nb = nsm;  // one CTA per SM (smem-bound); tasks are claimed dynamically
   if (nb > plan.nsweeps * plan.nk) nb = plan.nsweeps * plan.nk;
-  k9_band<M><<<nb, RT, R2Layout<M>::bytes, st>>>(f, rhs, ctx, err, plan);
+  k9_band<M, BW><<<nb, RT, R2Layout<M, BW>::bytes, st>>>(f, rhs, ctx, err, plan);
 }
 
 }  // namespace rb

@@ -53,14 +53,16 @@ __device__ __forceinline__ void store_rec(double* __restrict__ p, const double (
   if (N & 1) __stcs(p + N - 1, v[N - 1]);
 }
 
-// project (projection.hpp:64-89) of a stride-1 row in place
-template <int M>
+// project (projection.hpp:64-89) of a stride-1 row in place.  SKIP = false
+// runs every axis pass (an identity pass when the axis' shift is zero: the
+// same values), which keeps the code straight-line for the large orders.
+template <int M, bool SKIP = true>
 __device__ __forceinline__ void project_row(double* v, const P4& from, const P4& to) {
   const double b2 = -(to.v[3] - from.v[3]);
   const bool ds = to.v[3] != from.v[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    if (!ds && to.v[d] == from.v[d]) continue;
+    if (SKIP && !ds && to.v[d] == from.v[d]) continue;
     const double a = -(to.v[d] - from.v[d]);
     double c[M + 1];
     c[0] = 1.0;
@@ -75,7 +77,7 @@ __device__ __forceinline__ void project_row(double* v, const P4& from, const P4&
 
 // grad_normalize (projection.hpp:96-121) of a stride-1 row; rep_velocity /
 // rep_temperature / grad_defect (moment_rep.hpp:69-110), 2e_d at 4, 7, 9
-template <int M>
+template <int M, bool SKIP = true>
 __device__ __forceinline__ int normalize_row(double* v, P4& prm, double* bad) {
   for (int iter = 0; iter < 30; ++iter) {
     const double rho = v[0];
@@ -108,7 +110,7 @@ __device__ __forceinline__ int normalize_row(double* v, P4& prm, double* bad) {
       return W_GRAD_THETA;
     }
     if (!isfinite(to.v[0]) || !isfinite(to.v[1]) || !isfinite(to.v[2])) return W_GRAD_U;
-    project_row<M>(v, prm, to);
+    project_row<M, SKIP>(v, prm, to);
     prm = to;
   }
   double defect = 0.0, trace = 0.0;

@@ -29,6 +29,11 @@ CASES = [
     (3, SHAKHOV, 130, 20, (3, 2, 1, 0), False, 2),
     (5, BGK, 66, 40, (3, 1, 0, 2), True, 1),
     (4, SHAKHOV, 33, 90, (0, 3, 2, 1), True, 1),
+    # M = 6: the same kernel with 16-column bands and the flux in place in shared memory (BASELINE C4's order)
+    (6, BGK, 50, 37, (0, 1, 2, 3), False, 2),
+    (6, SHAKHOV, 40, 21, (2, 3, 0, 1), True, 2),
+    (6, BGK, 35, 18, (1, 0, 3, 2), True, 1),
+    (6, BGK, 20, 33, (3, 2, 1, 0), False, 1),
 ]
 
 

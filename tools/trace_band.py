@@ -21,7 +21,7 @@ c, p = c5_field(n, n, M, seed=1)
 f = momg.CellField.from_host(g, M, c, p)
 momg.fast_sweep_step(f, None, ctx)
 L = momg.lib()
-bw = 32
+bw = 16 if M == 6 else 32
 nb = (n + bw - 1) // bw
 cap = 4 * nb
 L.momg_debug_trace(C.c_longlong(4 * cap))
