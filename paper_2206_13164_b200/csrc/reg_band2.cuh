@@ -255,9 +255,14 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
     if (warp == 2 && has_rhs) rhs_project<M, BW>(rhsf, b, dfirst, PO + (dfirst & 3) * PS, R);
     __syncthreads();
     if (tr) t0 = sp::gtimer();
-    // face of this warp: fw = warp >> 1 (0 x-upstream, 1 x-downstream, 2
-    // y-upstream, 3 y-downstream in the sweep's rotated frame), side = warp & 1
-    const int fw = warp >> 1, side = warp & 1, axis = fw >> 1;
+    // face of this warp: fw (0 x-upstream, 1 x-downstream, 2 y-upstream, 3
+    // y-downstream in the sweep's rotated frame) and side.  32-column bands:
+    // fw = warp >> 1, side = warp & 1, lane = cell.  16-column bands (PAIR):
+    // both sides of a face in ONE warp, lane = cell + 16 side, so warps 0..3
+    // run the four faces with every lane busy (the sides differ by selects
+    // only) instead of eight half-empty warps.
+    constexpr bool PAIR = BW == 16;
+    const int fw = PAIR ? (warp & 3) : warp >> 1, side = PAIR ? (c >> 4) : (warp & 1), axis = fw >> 1;
     const bool upf = (fw & 1) == 0;
     const bool a_up = axis == 0 ? b.i_up : b.j_up;
     const bool high = upf ? !a_up : a_up;  // the rotated upstream face is the low face of an ascending axis
@@ -272,7 +277,13 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
       const int jr = d - ir;
       const bool valid = c < BW && ir < f.nx && jr >= 0 && jr < f.ny;
       // ---- (A) faces: this warp's side of its face for the 32 cells
-      {
+      if (!PAIR || warp < 4) {
+        // (inside this block c, ir, jr, valid are the face thread's cell: lane & 15 when PAIR)
+        const int lane_ = c, ir_ = ir;
+        const int c = PAIR ? (lane_ & 15) : lane_;
+        const int ir = PAIR ? BW * k + c : ir_;
+        const int jr = d - ir;
+        const bool valid = c < BW && ir < f.nx && jr >= 0 && jr < f.ny;
         // the cell at rotated offset r along the axis: (c + r, d + r) for
         // x, (c, d + r) for y; new ring below the diagonal, old ring above
         auto at = [&](int r, const double** v, const double** pp) {
