@@ -253,15 +253,19 @@ int momg_strips_scatter(momg_strips* s, int which, const momg_field* full, momg_
 
 /* ---- execution strategy of fast_sweep (same results either way) -------- */
 /* 1 (default): one persistent dataflow kernel per call (the band kernels for
-   M <= 5, thread-per-face M = 6, warp-per-cell M = 7, 8); 2: the same without
+   M <= 6 -- residuals and ES-BGK of M = 6 thread-per-face --, warp-per-cell
+   M = 7, 8); 2: the same without
    the band kernels (thread-per-face / warp-per-cell for every M); 0: one launch
    per anti-diagonal (the simple reference strategy; env MOMG_SWEEP=diag). */
 int momg_set_sweep_mode(int mode);
-/* band kernel of the first-order exact sweeps and residuals (M <= 5): 1
-   (default; env MOMG_RB=0 selects 0) the register-resident kernel (one thread
-   per face side, moment vectors in registers); 0 the split kernel (each face
-   cut 4 ways across warps through shared memory).  Results agree to rounding
-   (the two halves of a face flux are summed after the back projection). */
+/* band kernel of the exact-order sweeps (first / second order, with or
+   without an FAS right-hand side) and first-order residuals: 1 (default; env
+   MOMG_RB=0 selects 0) the register-resident kernels (one thread per face
+   side, moment vectors in registers: k8_band, k9_band; M <= 5 on 32-column
+   bands, M = 6 on 16-column bands); 0 the split kernels of M <= 5 (each face
+   cut 4 ways across warps through shared memory; thread-per-face for M = 6).
+   Results agree to rounding (the two halves of a face flux are summed after
+   the back projection). */
 int momg_set_band_kernel(int kind);
 
 /* ---- instrumentation --------------------------------------------------- */

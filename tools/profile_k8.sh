@@ -34,6 +34,13 @@ python tools/launch_summary.py gpurun_out/r2_k9_nmg_launches.csv \
   "# ncu launch list, C2 NMG V-cycles (tools/prof_nmg.py; k9_band = second-order / rhs register-resident band sweep)" \
   > gpurun_out/r2_k9_nmg_launches_summary.txt
 python tools/trace_band.py 128 5 2 > gpurun_out/r2_k9_trace_128.txt 2>&1
+# 3c) M = 6 (k9_band<6,16>, BASELINE C4's order): one 16-column band, and the step trace at 512^2
+python tools/prof_band.py --M 6 --order 2 --nx 16 --ny 512 > gpurun_out/plain_band_k9m6.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k9_band" -c 1 \
+    -o /tmp/band_k9m6 -f python tools/prof_band.py --M 6 --order 2 --nx 16 --ny 512 > gpurun_out/ncu_band_k9m6.log 2>&1
+python tools/ncu_summary.py /tmp/band_k9m6.ncu-rep k9_band 40 > gpurun_out/r2_ncu_k9m6_summary.txt 2>&1
+python tools/ncu_lines.py /tmp/band_k9m6.ncu-rep 50 > gpurun_out/r2_ncu_k9m6_lines.txt 2>&1
+python tools/trace_band.py 512 6 2 > gpurun_out/r2_k9m6_trace_512.txt 2>&1
 # 4) band step trace at 2048^2 (per-phase %globaltimer stamps, not timed)
 python tools/trace_band.py 2048 > gpurun_out/r2_k8_trace_2048.txt 2>&1
 echo profile done
