@@ -386,6 +386,51 @@ __device__ __forceinline__ unsigned band_counters_ahead(const Addr& fld, const G
   return ahead;
 }
 
+// apply_update (single_level.cpp:44-62) of one cell in registers: f + dt
+// delta, grad_normalize, the dt/2 retry; the new state into Vout / PVout.
+// Returns the failure kind (W_NONE: ok).  For the large orders this is an
+// out-of-line function, so that its 2 N-register vector is allocated apart
+// from the kernel's loop-carried state.
+template <int M>
+__device__ __forceinline__ int cell_update_body(const double* S, const double* D, const double* cpp, double dt,
+                                                double* Vout, double* PVout, double* bad) {
+  constexpr int N = Gen<M>::N;
+  double v[N];
+  const P4 cp = pload(cpp);
+  P4 prm = cp;
+  int fail = W_NONE;
+  bool good = false;
+#pragma unroll 1
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const double h = attempt ? 0.5 * dt : dt;
+    asm volatile("" ::: "memory");
+#pragma unroll
+    for (int kk = 0; kk < N; ++kk) v[kk] = S[kk * SPV] + h * D[kk * SPV];
+    prm = cp;
+    const int st = xf::normalize_row<M, (M <= 5)>(v, prm, bad);
+    if (st == W_NONE) {
+      good = true;
+      break;
+    }
+    if (st != W_GRAD_RHO && st != W_GRAD_THETA && st != W_GRAD_U) {  // plain Error (cap)
+      fail = st;
+      break;
+    }
+    if (attempt == 1) fail = W_DT_HALVING;  // SolverError after the dt/2 retry
+  }
+  if (fail == W_NONE && good) {
+    vstore<M>(Vout, v);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) PVout[t] = prm.v[t];
+  }
+  return fail;
+}
+template <int M>
+__device__ __noinline__ int cell_update_call(const double* S, const double* D, const double* cpp, double dt,
+                                             double* Vout, double* PVout, double* bad) {
+  return cell_update_body<M>(S, D, cpp, dt, Vout, PVout, bad);
+}
+
 // Coalesced write-back of nc cells starting at c0 of diagonal dd (new states
 // V[dd & 1], bases PV, only cells whose update succeeded); lane = coefficient.
 template <int M, class Geo>
@@ -595,48 +640,17 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
       // ---- (C) warp 0: the cell update (sweep) / the residual stores (res);
       // the others: publish d-1, scalars of d+1, old(d+2), band k-1's halo
       if (warp == 0 && !res) {
-        double v[N];
-        const double* S = O + o0 * VEC + c;
-        const double* D = smem + LY::V_F * VEC + c;
-        const P4 cp = pload(PO + o0 * 132 + c * 4);
-        P4 prm = cp;
         int fail = pfail;
-        bool good = false;
         double bad = 0.0;
-        if (valid && fail == W_NONE) {
-          const double dt = pre[sp::PRE_DT * 32];
-#pragma unroll 1
-          for (int attempt = 0; attempt < 2; ++attempt) {
-            const double h = attempt ? 0.5 * dt : dt;
-            // (the clobber keeps S and D from being held in registers across
-            // the rare retry: they are re-read from shared memory)
-            asm volatile("" ::: "memory");
-#pragma unroll
-            for (int kk = 0; kk < N; ++kk) v[kk] = S[kk * SPV] + h * D[kk * SPV];
-            prm = cp;
-            const int st = xf::normalize_row<M>(v, prm, &bad);
-            if (st == W_NONE) {
-              good = true;
-              break;
-            }
-            if (st != W_GRAD_RHO && st != W_GRAD_THETA && st != W_GRAD_U) {  // plain Error (cap)
-              fail = st;
-              break;
-            }
-            if (attempt == 1) fail = W_DT_HALVING;  // SolverError after the dt/2 retry
-          }
-        }
+        if (valid && fail == W_NONE)
+          fail = cell_update_body<M>(O + o0 * VEC + c, smem + LY::V_F * VEC + c, PO + o0 * 132 + c * 4,
+                                     pre[sp::PRE_DT * 32], smem + (LY::V_V + (d & 1)) * VEC + c,
+                                     smem + LY::PV + (d & 1) * 132 + c * 4, &bad);
         if (valid && fail) {
           const int i = b.i_up ? ir : f.nx - 1 - ir, j = b.j_up ? jr : f.ny - 1 - jr;
           tc::raise(err, tc::code_for(fail), fail, i, j, bad);
         }
-        const bool ok = valid && fail == W_NONE && good;
-        if (ok) {
-          vstore<M>(smem + (LY::V_V + (d & 1)) * VEC + c, v);
-          double* pv = smem + LY::PV + (d & 1) * 132 + c * 4;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) pv[t] = prm.v[t];
-        }
+        const bool ok = valid && fail == W_NONE;
         s_ok[d & 1][c] = ok ? 1 : 0;
         if (tr) s_tr[4] += sp::gtimer() - s_tr[0];
       } else if (res && warp <= 1) {

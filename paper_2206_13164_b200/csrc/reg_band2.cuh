@@ -513,46 +513,23 @@ __global__ void __launch_bounds__(RT, 1) k9_band(DevField f, DevField rhsf, DevC
       // d+1, publication of d-2 and write-back of d-1, the copy of old(d+3),
       // band k-1's new cells of diagonal d
       if (warp == 0) {
-        double v[N];
-        const double* S = O + (d & 3) * VEC + c;
-        const double* D = smem + LY::V_F * VEC + c;
-        const P4 cp = pload(PO + (d & 3) * PS + c * 4);
-        P4 prm = cp;
         int fail = pfail;
-        bool good = false;
         double bad = 0.0;
         if (valid && fail == W_NONE) {
+          const double* S = O + (d & 3) * VEC + c;
+          const double* D = smem + LY::V_F * VEC + c;
+          const double* cpp = PO + (d & 3) * PS + c * 4;
+          double* Vout = V + (d & 1) * VEC + c + 2;
+          double* PVout = PV + (d & 1) * PS + (c + 2) * 4;
           const double dt = pre[sp::PRE_DT * 32];
-#pragma unroll 1
-          for (int attempt = 0; attempt < 2; ++attempt) {
-            const double h = attempt ? 0.5 * dt : dt;
-            asm volatile("" ::: "memory");
-#pragma unroll
-            for (int kk = 0; kk < N; ++kk) v[kk] = S[kk * SPV] + h * D[kk * SPV];
-            prm = cp;
-            const int st = xf::normalize_row<M, (M <= 5)>(v, prm, &bad);
-            if (st == W_NONE) {
-              good = true;
-              break;
-            }
-            if (st != W_GRAD_RHO && st != W_GRAD_THETA && st != W_GRAD_U) {  // plain Error (cap)
-              fail = st;
-              break;
-            }
-            if (attempt == 1) fail = W_DT_HALVING;  // SolverError after the dt/2 retry
-          }
+          if constexpr (M <= 5) fail = cell_update_body<M>(S, D, cpp, dt, Vout, PVout, &bad);
+          else fail = cell_update_call<M>(S, D, cpp, dt, Vout, PVout, &bad);
         }
         if (valid && fail) {
           const int i = b.i_up ? ir : f.nx - 1 - ir, j = b.j_up ? jr : f.ny - 1 - jr;
           tc::raise(err, tc::code_for(fail), fail, i, j, bad);
         }
-        const bool ok = valid && fail == W_NONE && good;
-        if (ok) {
-          vstore<M>(V + (d & 1) * VEC + c + 2, v);
-          double* pv = PV + (d & 1) * PS + (c + 2) * 4;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) pv[t] = prm.v[t];
-        }
+        const bool ok = valid && fail == W_NONE;
         s_ok[d & 1][c] = ok ? 1 : 0;
         if (tr) s_tr[4] += sp::gtimer() - s_tr[0];
       } else if (warp == 1) {
