@@ -393,7 +393,7 @@ __device__ __forceinline__ unsigned band_counters_ahead(const Addr& fld, const G
 // from the kernel's loop-carried state.
 template <int M>
 __device__ __forceinline__ int cell_update_body(const double* S, const double* D, const double* cpp, double dt,
-                                                double* Vout, double* PVout, double* bad) {
+                                                double* Vout, double* PVout, double* bad, int& tries) {
   constexpr int N = Gen<M>::N;
   double v[N];
   const P4 cp = pload(cpp);
@@ -403,6 +403,7 @@ __device__ __forceinline__ int cell_update_body(const double* S, const double* D
 #pragma unroll 1
   for (int attempt = 0; attempt < 2; ++attempt) {
     const double h = attempt ? 0.5 * dt : dt;
+    tries = attempt + 1;
     asm volatile("" ::: "memory");
 #pragma unroll
     for (int kk = 0; kk < N; ++kk) v[kk] = S[kk * SPV] + h * D[kk * SPV];
@@ -424,6 +425,12 @@ __device__ __forceinline__ int cell_update_body(const double* S, const double* D
     for (int t = 0; t < 4; ++t) PVout[t] = prm.v[t];
   }
   return fail;
+}
+template <int M>
+__device__ __forceinline__ int cell_update_body(const double* S, const double* D, const double* cpp, double dt,
+                                                double* Vout, double* PVout, double* bad) {
+  int tries = 0;
+  return cell_update_body<M>(S, D, cpp, dt, Vout, PVout, bad, tries);
 }
 template <int M>
 __device__ __noinline__ int cell_update_call(const double* S, const double* D, const double* cpp, double dt,
@@ -474,8 +481,9 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
   __shared__ int s_task, s_stop;
   __shared__ int s_ok[2][32];
   // debug trace accumulators: [0] step start, [1] write-back, [2] faces, [3] assembled, [4] updated, [5] end;
-  // s_wA / s_wC: per-warp arrival at the face / end-of-step barrier
-  __shared__ unsigned long long s_tr[6], s_wA[8], s_wC[8], s_wM[8];
+  // s_wA: histogram of the step durations; s_wC: per-warp arrival at the end-of-step barrier;
+  // s_retry: steps with a dt/2 retry | steps with an update > 3 us << 32; s_b: barrier (B) of the step
+  __shared__ unsigned long long s_tr[6], s_wA[8], s_wC[8], s_wM[8], s_retry, s_b;
   const int tid = threadIdx.x, warp = tid >> 5, c = tid & 31;
   const int sweep_tasks = RES ? 0 : plan.nsweeps * plan.nk;
   const int ntasks = sweep_tasks + plan.nchunks * plan.nk;
@@ -519,10 +527,12 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
     const bool trw = plan.trace && 4 * task + 3 < plan.trace_cap && c == 0;
     const bool tr = trw && tid == 0;
     unsigned long long t0 = 0;
+    long long c0 = 0;
     if (trw) {
       s_wA[warp] = s_wC[warp] = s_wM[warp] = 0;
       if (tid == 0)
         for (int q = 0; q < 6; ++q) s_tr[q] = 0;
+      if (tid == 0) s_retry = s_b = 0;
     }
     // ---- prologue: warp 0 waits (with back-off) for the first two diagonals
     // and band k-1's halo cell; then O <- old(dfirst), old(dfirst+1), halo
@@ -567,7 +577,10 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
       sp::band_pre<M, BW>(f, ctx, b, dfirst, O + (dfirst & 3) * VEC, PO + (dfirst & 3) * 132,
                           smem + LY::PRE + (dfirst & 1) * sp::PRE_N * 32);
     __syncthreads();
-    if (tr) t0 = sp::gtimer();
+    if (tr) {
+      t0 = sp::gtimer();
+      c0 = clock64();
+    }
     // face of this warp: f = warp >> 1 (0 x-upstream, 1 x-downstream, 2 y-up,
     // 3 y-down in the sweep's rotated frame), side = warp & 1
     const int fw = warp >> 1, side = warp & 1, axis = fw >> 1;
@@ -617,7 +630,6 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
           tc::raise(err, tc::code_for(w), w, i, j, 0.0);
         }
       }
-      if (trw) s_wA[warp] += sp::gtimer() - s_tr[0];
       __syncthreads();
       if (tr) s_tr[2] += sp::gtimer() - s_tr[0];
       // ---- (B) residual assembly, coefficients split over the 8 warps (D in F[0])
@@ -636,16 +648,27 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
         }
       }
       __syncthreads();
-      if (tr) s_tr[3] += sp::gtimer() - s_tr[0];
+      if (tr) {
+        s_b = sp::gtimer() - s_tr[0];
+        s_tr[3] += s_b;
+      }
       // ---- (C) warp 0: the cell update (sweep) / the residual stores (res);
       // the others: publish d-1, scalars of d+1, old(d+2), band k-1's halo
       if (warp == 0 && !res) {
         int fail = pfail;
         double bad = 0.0;
+        int tries = 0;
         if (valid && fail == W_NONE)
           fail = cell_update_body<M>(O + o0 * VEC + c, smem + LY::V_F * VEC + c, PO + o0 * 132 + c * 4,
                                      pre[sp::PRE_DT * 32], smem + (LY::V_V + (d & 1)) * VEC + c,
-                                     smem + LY::PV + (d & 1) * 132 + c * 4, &bad);
+                                     smem + LY::PV + (d & 1) * 132 + c * 4, &bad, tries);
+        if (plan.trace) {  // (debug trace) steps with a dt/2 retry, steps whose update took > 3 us
+          const bool any2 = __any_sync(0xffffffffu, tries > 1);
+          if (tr) {
+            if (any2) s_retry += 1ull;
+            if (sp::gtimer() - s_tr[0] - s_b > 3000) s_retry += 1ull << 32;
+          }
+        }
         if (valid && fail) {
           const int i = b.i_up ? ir : f.nx - 1 - ir, j = b.j_up ? jr : f.ny - 1 - jr;
           tc::raise(err, tc::code_for(fail), fail, i, j, bad);
@@ -745,7 +768,14 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
       }
       if (trw) s_wC[warp] += sp::gtimer() - s_tr[0];
       __syncthreads();
-      if (tr) s_tr[5] += sp::gtimer() - s_tr[0];
+      if (tr) {
+        const unsigned long long dur = sp::gtimer() - s_tr[0];
+        s_tr[5] += dur;
+        // histogram of the step durations (bins end at 9, 10, 11, 12.5, 15, 20, 40 us, then the rest)
+        const int bin = dur < 9000 ? 0 : dur < 10000 ? 1 : dur < 11000 ? 2 : dur < 12500 ? 3 : dur < 15000 ? 4
+                        : dur < 20000 ? 5 : dur < 40000 ? 6 : 7;
+        s_wA[bin] += 1;
+      }
       if (s_stop) return;
     }
     if (!res) rb_writeback<M>(f, b, dlast, smem + (LY::V_V + (dlast & 1)) * VEC, smem + LY::PV + (dlast & 1) * 132,
@@ -776,7 +806,8 @@ __global__ void __launch_bounds__(RT, 1) k8_band(DevField f, DevCtx ctx, DevErr*
       o[10] = 0;  // (marks the k8 stamp set; warp 4's mid-role stamp is not kept)
       o[12] = s_tr[3];
       o[14] = s_wM[6];
-
+      o[6] = s_retry;  // steps with a dt/2 retry | steps with an update > 3 us << 32
+      o[15] = (unsigned long long)(clock64() - c0);  // SM cycles over the loop (effective clock)
     }
   }
 }

@@ -39,7 +39,15 @@ if np.sum(t[:, 10]) == 0:  # register-resident kernel (k8_band): its own stamp s
     print("k8_band per-step means, us from step start: write-back %.2f  faces(barrier A) %.2f  assembled(barrier B) %.2f"
           "  updated(warp 0) %.2f  end(barrier C) %.2f;  loop time/step %.2f"
           % (m(3), m(4), m(12), m(5), m(7), np.sum(t[:, 1] - t[:, 0]) / S / 1e3))
-    print("per-warp arrival at barrier A:", " ".join("%.2f" % m(16 + w) for w in range(8)))
+    print("step durations, share of steps in bins <9 <10 <11 <12.5 <15 <20 <40 >=40 us: all tasks",
+          " ".join("%.3f" % (np.sum(t[:, 16 + w]) / S) for w in range(8)))
+    rt = buf[:got, 6]
+    print("steps with a dt/2 retry in the warp: %.4f   steps with an update > 3 us: %.4f"
+          % (np.sum(rt & 0xffffffff) / S, np.sum(rt >> 32) / S))
+    for r in (0, 1, 4, 8, 16, 32, 48, 63, 64, 80, 127, 128, 192, 255):
+        if r < got:
+            print("   task %3d (s %d k %2d):" % (r, sk[r][0], sk[r][1]),
+                  " ".join("%.3f" % (t[r, 16 + w] / steps[r]) for w in range(8)))
     print("per-warp arrival at barrier C:", " ".join("%.2f" % m(24 + w) for w in range(8)))
     print("mid-role stamps, warps 2..7 (2-4 after the release, 5-6 after the cp.async issue, 7 after the halo poll):",
           " ".join("%.2f" % m(q) for q in (8, 9, 11, 14, 13)), "(warps 2, 3, 5, 6, 7)")
@@ -50,6 +58,21 @@ if np.sum(t[:, 10]) == 0:  # register-resident kernel (k8_band): its own stamp s
             q = np.array_split(np.array(rows_), 4)
             print(f"sweep {sw}: us/step by band quarter:", " ".join("%.2f" % ups[x].mean() for x in q if len(x)),
                   "| start %.1f ms end %.1f ms" % ((t[rows_, 0].min() - t0) / 1e6, (t[rows_, 1].max() - t0) / 1e6))
+    # per sweep and band quarter: the phases of the step and the SM clock the loop saw
+    # (load dependence: the bands at both ends of the launch run with fewer active SMs)
+    print("sweep.quarter: active-window ms | faces  B  update  tail  step (us) | SM MHz")
+    for sw in range(4):
+        rows_ = np.array([r for r in range(got) if sk[r][0] == sw])
+        if not len(rows_):
+            continue
+        for qi, x in enumerate(np.array_split(rows_, 4)):
+            if not len(x):
+                continue
+            Sx = np.sum(steps[x])
+            mq = lambda q: np.sum(t[x, q]) / Sx / 1e3
+            mhz = np.sum(t[x, 15]) / np.maximum(np.sum(t[x, 1] - t[x, 0]), 1) * 1e3
+            print(f"  {sw}.{qi}: {(t[x, 0].min() - t0) / 1e6:6.1f}-{(t[x, 1].max() - t0) / 1e6:6.1f} | "
+                  f"{mq(4):5.2f} {mq(12) - mq(4):5.2f} {mq(5) - mq(12):5.2f} {mq(7) - mq(5):5.2f} {mq(7):6.2f} | {mhz:5.0f}")
     print(" task  s   k  loop(us)  end(us)  steps  us/step")
     for r in (list(range(0, min(4, got))) + list(range(nb - 2, nb + 2)) + list(range(got - 3, got))):
         if 0 <= r < got:
