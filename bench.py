@@ -365,7 +365,8 @@ def ours(a):
                "mode": "double-buffered stream of solves: the H2D of step i+1 is enqueued before step i and "
                        "the D2H of step i after it, on the library's copy streams (pinned host buffers, C ABI "
                        "*_overlapped calls with a deferred per-field wait); ms_per_step vs the device-timed "
-                       "ms_per_step shows what the copies cost"}
+                       "ms_per_step shows what the copies cost (the first upload and the last download are "
+                       "not hidden: pipeline fill and drain, amortised over the K timed steps)"}
 
     # ---- NMG time-to-1e-8 on C2 (128^2, M=5, order 2, 4 levels)
     nmg = None

@@ -426,6 +426,15 @@ bool band_sweep_enabled();
 // the register-resident band kernel (reg_band.cuh) for first-order exact
 // sweeps / residuals of M <= 5 (momg_set_band_kernel: 1 default, 0 k5_band)
 bool rb_enabled();
+// Resident CTAs of a register-resident band sweep: the exact order keeps
+// ~0.8 nk band tasks running (nk = bands per sweep), the CTAs beyond that hold
+// tasks that wait for their first dependency.  Two CTAs on the SMs of one TPC
+// slow each other down (the 155 KB step loop streams through the shared
+// instruction path: 2048^2 fused launch 122 ms at 148 CTAs, 96-98 ms at
+// 88-100; the waiting CTAs' polling is not the cause: a 8x longer back-off
+// changes nothing), so the grid is capped at min(1.5 nk, 0.65 SMs) and the
+// hardware spreads it over the TPCs first.  MOMG_RB_GRID overrides the cap.
+int rb_grid_cap(int nb, int nk);
 
 // rb::k9_band (reg_band2.cuh, own translation units rb2_m<M>.cu)
 void rb2_launch_m3(const DevField& f, const DevField& rhs, const DevCtx& ctx, DevErr* err, const sp::BandPlan& plan,
@@ -448,6 +457,7 @@ void rb_launch(const DevField& f, const DevCtx& ctx, const sp::BandPlan& bp, con
   int nb = tc_sweep_blocks((const void*)rb::k8_band<M, RES>, rb::RLayout<M>::bytes, rb::RT);
   const int tasks = (RES ? 0 : bp.nsweeps * bp.nk) + bp.nchunks * bp.nk;
   if (nb > tasks) nb = tasks;
+  if (!RES) nb = rb_grid_cap(nb, bp.nk);
   if (nb < 1) nb = 1;
   rb::k8_band<M, RES><<<nb, rb::RT, rb::RLayout<M>::bytes, momg_rt::stream()>>>(f, ctx, momg_rt::err_dev(), bp,
                                                                                    out);

@@ -33,6 +33,7 @@
 #include "reg_band.cuh"
 
 namespace momg_gpu {
+int rb_grid_cap(int nb, int nk);  // runtime.cu (declared with its rationale in kernels_impl.cuh)
 namespace rb {
 
 
@@ -612,6 +613,7 @@ void rb2_launch_impl(const DevField& f, const DevField& rhs, const DevCtx& ctx, 
   }
   int nb = nsm;  // one CTA per SM (smem-bound); tasks are claimed dynamically
   if (nb > plan.nsweeps * plan.nk) nb = plan.nsweeps * plan.nk;
+  nb = rb_grid_cap(nb, plan.nk);  // (kernels_impl.cuh: one CTA per TPC while the tasks allow it)
   k9_band<M, BW><<<nb, RT, R2Layout<M, BW>::bytes, st>>>(f, rhs, ctx, err, plan);
 }
 

@@ -550,6 +550,26 @@ bool rb_enabled() {
 }
 void set_rb_mode(int m) { g_rb = m; }
 
+int rb_grid_cap(int nb, int nk) {
+  static const int env = [] {
+    const char* e = getenv("MOMG_RB_GRID");
+    return e ? atoi(e) : 0;
+  }();
+  static const int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  // 1.5 nk running + waiting tasks, and at most ~2/3 of the SMs: beyond that the
+  // second CTA of a TPC costs more than its task gains (4096^2: 290 ms at 96
+  // CTAs, 314 ms at 148, 361 ms at 64)
+  int cap = (3 * nk + 1) / 2;
+  const int tpc = (sms * 13) / 20;
+  if (cap > tpc) cap = tpc;
+  if (env > 0) cap = env;
+  return nb < cap ? nb : (cap < 1 ? 1 : cap);
+}
 int tc_sweep_blocks(const void* kernel, size_t smem, int threads) {
   int per_sm = 0, dev = 0, sms = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
